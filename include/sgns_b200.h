@@ -1,0 +1,137 @@
+/*
+ * sgns_b200.h -- C ABI of the B200-native pSGNScc hot path.
+ *
+ * All pointers named d_* are device pointers (HBM); h_* are host pointers.
+ * Every device entry point is stream-ordered on `stream` (a cudaStream_t
+ * passed as void*), allocates nothing, and returns 0 or a status:
+ *   > 0  a cudaError_t from the launch,
+ *   < 0  SGNS_E_* validation errors below.
+ * No torch types cross this boundary; INTEGRATION.md shows the ctypes
+ * binding the reference package would add.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/sgns):
+ *   sgns_update_windows  <- batch_core_blas / batch_core_naive
+ *                           (kernel_batched.py:92-144, :147-211) behind
+ *                           process_batch (kernel_batched.py:214-260)
+ *   sgns_drive           <- _drive_batched (trainer.py:217-311) behind
+ *                           ThreadRun.advance(word_budget) (trainer.py:396-442);
+ *                           includes _subsample (corpus.py:168-181), the window
+ *                           assembly (trainer.py:260-280), chunking and
+ *                           fill_shared_negatives (kernel_batched.py:57-66)
+ *   sgns_init_model      <- init_model (model.py:64-74)
+ *   sgns_expand_slots    <- build_negative_table's slot array (corpus.py:139-155)
+ *   sgns_build_alias     <- (new) Vose alias table over count^0.75, the
+ *                           production replacement of the 10^8-slot table
+ */
+#ifndef SGNS_B200_H
+#define SGNS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGNS_ABI_VERSION 1
+
+enum {
+  SGNS_OK = 0,
+  SGNS_E_ARG = -1,       /* bad argument (null pointer, size, mode) */
+  SGNS_E_SHAPE = -2,     /* dim / window / K / batch_cap outside the supported envelope */
+  SGNS_E_SMEM = -3,      /* per-warp staging does not fit in shared memory */
+  SGNS_E_DEVICE = -4     /* device-side validation failed (see sgns_error_string) */
+};
+
+enum { SGNS_F32 = 0, SGNS_F64 = 1 };
+enum { SGNS_SIGMOID_TABLE = 0, SGNS_SIGMOID_EXACT = 1 };
+enum { SGNS_RNG_SPLITMIX = 0, SGNS_RNG_PHILOX = 1 };
+
+/* Per-worker resumable state (one worker = one warp = one reference thread,
+ * ThreadRun fields trainer.py:358-366, alpha_state :365). Device resident. */
+typedef struct sgns_worker {
+  int64_t next_sent, lo, hi;
+  int32_t epoch, done;
+  uint64_t rng;                       /* splitmix64 state (SGNS_RNG_SPLITMIX) */
+  double alpha, read_local, trained_local;
+  int64_t kernel_counter, words_read, words_trained;
+} sgns_worker;
+
+/* One batch of packed windows (the CSR form of a list of Minibatch,
+ * kernel_batched.py:37-54): window w has inputs in_ids[in_off[w]:in_off[w+1]]
+ * and outputs out_ids[w*k1 : (w+1)*k1], target first. */
+int sgns_update_windows(
+    int32_t dtype,
+    void *d_m_in_dst, void *d_m_out_dst,              /* rows receive += deltas */
+    const void *d_m_in_src, const void *d_m_out_src,  /* rows are gathered from here */
+    int64_t vocab, int32_t dim, int64_t ld,           /* ld: row stride in elements, multiple of 16 B */
+    const int32_t *d_in_off, const int32_t *d_in_ids, const int32_t *d_out_ids,
+    int32_t n_windows, int32_t k1, int32_t max_inputs,
+    const void *d_alpha,                              /* per window, model dtype */
+    const void *d_sig_table,                          /* 1000 entries, model dtype */
+    int32_t sigmoid_mode, int32_t loss_every,
+    double *d_loss_sum, int64_t *d_loss_cells,        /* may be NULL when loss_every == 0 */
+    int32_t *d_error,                                 /* may be NULL */
+    void *stream);
+
+typedef struct sgns_drive_params {
+  int32_t dtype;
+  void *d_m_in, *d_m_out;
+  int64_t vocab, ld;
+  int32_t dim;
+  const int32_t *d_ids;          /* corpus token ids */
+  const int64_t *d_offsets;      /* sentence offsets, n_sentences + 1 */
+  const double *d_keep_probs;    /* NULL: no subsampling */
+  int32_t rng_mode;
+  const int32_t *d_slots;        /* SPLITMIX: reference slot table */
+  int64_t n_slots;
+  const uint32_t *d_alias_thr;   /* PHILOX: alias thresholds (x 2^32) */
+  const int32_t *d_alias_idx;
+  uint64_t seed;                 /* PHILOX key */
+  int32_t window, dynamic, k_neg, batch_cap, sigmoid_mode;
+  const void *d_sig_table;
+  double alpha0, floor_frac, total_x_epochs;
+  int64_t refresh_words;         /* ALPHA_REFRESH_WORDS (trainer.py:48) */
+  int64_t *d_shared;             /* [2] words read / trained, shared by all workers */
+  int32_t epochs, loss_every;
+  sgns_worker *d_workers;
+  int32_t n_workers;
+  int64_t word_budget;           /* per worker, words read (trainer.py:237) */
+  double *d_loss_by_epoch;       /* [n_workers * epochs] */
+  int64_t *d_cells_by_epoch;
+  int32_t update;                /* 0: draw / trace only */
+  int32_t max_sentence;          /* longest sentence in tokens (<= 1024) */
+  int64_t trace_cap;             /* records per worker; 0 disables tracing */
+  int32_t *d_trace;              /* [n_workers][trace_cap][4 + batch_cap + k1] */
+  double *d_trace_alpha;         /* [n_workers][trace_cap] */
+  int64_t *d_trace_count;        /* [n_workers] */
+  int32_t *d_error;              /* may be NULL */
+  int32_t warps_per_block;       /* 0: default */
+} sgns_drive_params;
+
+/* Fused resumable driver: every worker consumes up to word_budget words read. */
+int sgns_drive(const sgns_drive_params *p, void *stream);
+
+/* M_in ~ U(-0.5/dim, 0.5/dim) from the splitmix stream (seed, 0x1017), M_out = 0,
+ * padding columns [dim, ld) = 0.  Bit-identical to init_model. */
+int sgns_init_model(int32_t dtype, void *d_m_in, void *d_m_out, int64_t vocab, int32_t dim,
+                    int64_t ld, uint64_t seed, void *stream);
+
+/* slots[s] = word owning slot s given build_negative_table's boundaries. */
+int sgns_expand_slots(const int64_t *d_boundaries, int64_t vocab, int32_t *d_slots,
+                      int64_t n_slots, void *stream);
+
+/* Host: Vose alias table over count^power (float64). thr[i] = floor(p_i * 2^32). */
+int sgns_build_alias(const int64_t *h_counts, int64_t vocab, double power,
+                     uint32_t *h_thr, int32_t *h_alias);
+
+/* Occupancy-derived worker count: resident warps of the driver kernel. */
+int sgns_resident_workers(int32_t dtype, int32_t dim, int32_t window, int32_t k_neg,
+                          int32_t batch_cap, int32_t max_sentence, int32_t *out_workers);
+
+const char *sgns_error_string(int32_t code);
+int sgns_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGNS_B200_H */

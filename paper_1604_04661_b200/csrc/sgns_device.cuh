@@ -1,0 +1,377 @@
+// sgns_device.cuh -- device building blocks of the pSGNScc hot path (sm_100a).
+//
+// One warp = one worker.  A window (one chunk of <= batch_cap inputs sharing
+// the target + K negatives) is processed by one warp:
+//   1. gather: every lane cp.async's its 16-byte column chunks of the m input
+//      rows (M_in) and k1 output rows (M_out) into the warp's shared slab
+//      (all rows land before any write: the snapshot semantics of
+//      kernel_batched.py:104-113),
+//   2. scores S = A C^T: lane-local partial dots over its columns, then a
+//      transposed butterfly leaves each lane group one finished score,
+//   3. E = alpha (label - sigma(S)) with the reference's float64 bin-index
+//      rule (model.py:108-115) or the exact sigmoid (kernel_scalar.py:30-35),
+//   4. dA_i = alpha * sum_k err_ik C_k (register C) -> red.global.add.v4.f32,
+//      dC_k = sum_i (alpha err_ik) A_i (column-outer) -> red.global.add.v4.f32
+//      (kernel_batched.py:191-210, additive row application :135-143).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sgns {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+constexpr uint64_t kMix1 = 0xBF58476D1CE4E5B9ULL;
+constexpr uint64_t kMix2 = 0x94D049BB133111EBULL;
+constexpr uint32_t kTagSub = 0x53554230u;  // 'SUB0'
+constexpr uint32_t kTagWin = 0x57494E30u;  // 'WIN0'
+constexpr uint32_t kTagNeg = 0x4E000000u;
+constexpr int kSigBins = 1000;
+
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+  using type = float4;
+  static constexpr int N = 4;
+};
+template <> struct Vec<double> {
+  using type = double2;
+  static constexpr int N = 2;
+};
+
+// ---------------------------------------------------------------- RNG ----
+// splitmix64 exactly as rng.py:24-32; draw n of a stream in state s is
+// mix(s + (n+1) * golden), so a warp can evaluate 32 consecutive draws at once.
+__device__ __forceinline__ uint64_t sm_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * kMix1;
+  z = (z ^ (z >> 27)) * kMix2;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double u53(uint64_t z) {
+  return (double)(z >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// Philox4x32-10 (Salmon et al. 2011); counter = (token lo, token hi, epoch, tag).
+__device__ __forceinline__ uint4 philox(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+  }
+  return c;
+}
+__device__ __forceinline__ uint4 philox_tok(uint64_t tok, uint32_t epoch, uint32_t tag,
+                                            uint32_t k0, uint32_t k1) {
+  return philox(make_uint4((uint32_t)tok, (uint32_t)(tok >> 32), epoch, tag), k0, k1);
+}
+
+// ------------------------------------------------------------ helpers ----
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+__device__ __forceinline__ float4 vzero(float) { return make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ double2 vzero(double) { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ float vdot(const float4 &a, const float4 &b) {
+  return fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, a.x * b.x)));
+}
+__device__ __forceinline__ double vdot(const double2 &a, const double2 &b) {
+  return fma(a.y, b.y, a.x * b.x);
+}
+__device__ __forceinline__ void vfma(float4 &acc, float s, const float4 &v) {
+  acc.x = fmaf(s, v.x, acc.x);
+  acc.y = fmaf(s, v.y, acc.y);
+  acc.z = fmaf(s, v.z, acc.z);
+  acc.w = fmaf(s, v.w, acc.w);
+}
+__device__ __forceinline__ void vfma(double2 &acc, double s, const double2 &v) {
+  acc.x = fma(s, v.x, acc.x);
+  acc.y = fma(s, v.y, acc.y);
+}
+__device__ __forceinline__ void vscale(float4 &v, float s) {
+  v.x *= s; v.y *= s; v.z *= s; v.w *= s;
+}
+__device__ __forceinline__ void vscale(double2 &v, double s) {
+  v.x *= s; v.y *= s;
+}
+// Scatter-add one 16-byte chunk (no return value -> REDG.E.ADD.F32x4).
+__device__ __forceinline__ void red_add(float *p, const float4 &v) {
+  atomicAdd(reinterpret_cast<float4 *>(p), v);
+}
+__device__ __forceinline__ void red_add(double *p, const double2 &v) {
+  atomicAdd(p, v.x);
+  atomicAdd(p + 1, v.y);
+}
+
+// Transposed butterfly: NV partial sums per lane -> each lane ends with the
+// full warp sum of value index (lane >> (5 - log2 NV)) & (NV - 1).
+template <int NV> struct Log2 { static constexpr int v = 1 + Log2<NV / 2>::v; };
+template <> struct Log2<1> { static constexpr int v = 0; };
+
+template <int NV, typename T>
+__device__ __forceinline__ T transpose_reduce(T (&v)[NV], int lane) {
+  constexpr int L = Log2<NV>::v;
+#pragma unroll
+  for (int s = 0; s < L; ++s) {
+    const int half = NV >> (s + 1);
+    const int bit = 16 >> s;
+    const bool upper = (lane & bit) != 0;
+#pragma unroll
+    for (int q = 0; q < half; ++q) {
+      const T send = upper ? v[q] : v[q + half];
+      const T keep = upper ? v[q + half] : v[q];
+      v[q] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+    }
+  }
+#pragma unroll
+  for (int bit = 16 >> L; bit >= 1; bit >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], bit);
+  return v[0];
+}
+template <int NV> __device__ __forceinline__ int reduced_index(int lane) {
+  return (lane >> (5 - Log2<NV>::v)) & (NV - 1);
+}
+template <int NV> __device__ __forceinline__ int group_leader(int k) {
+  return k << (5 - Log2<NV>::v);
+}
+
+// model.py:108-115: idx = int((x + 6.0) * (1000.0 / 12.0)) in float64, clamped
+__device__ __forceinline__ int sig_index(double x) {
+  const double v = (x + 6.0) * (1000.0 / 12.0);
+  if (!(v >= 0.0)) return 0;
+  if (v >= 1000.0) return kSigBins - 1;
+  return __double2int_rz(v);
+}
+__device__ __forceinline__ double sig_exact(double x) {
+  if (x >= 0.0) return 1.0 / (1.0 + exp(-x));
+  const double ex = exp(x);
+  return ex / (1.0 + ex);
+}
+__device__ __forceinline__ double softplus(double x) {
+  return x > 0.0 ? x + log1p(exp(-x)) : log1p(exp(x));
+}
+
+template <typename T> struct ModelView {
+  T *in_dst;
+  T *out_dst;
+  const T *in_src;
+  const T *out_src;
+  int64_t ld;  // row stride in elements
+  int nvec;    // 16-byte chunks per row
+};
+
+// Per-cell error, as batch_core_naive computes it (kernel_batched.py:174-190):
+// label - sigma and alpha * err in float64, each rounded once to the model dtype.
+template <typename T>
+__device__ __forceinline__ void cell_error(T s, int k, T alpha, bool exact, const T *sig_s,
+                                           T &e_raw, T &e_scaled) {
+  const double sd = (double)s;
+  const T sig = exact ? (T)sig_exact(sd) : sig_s[sig_index(sd)];
+  const double err = (k == 0 ? 1.0 : 0.0) - (double)sig;
+  e_raw = (T)err;
+  e_scaled = (T)((double)alpha * err);
+}
+
+// ------------------------------------------------------ window update ----
+// ids_s: m input ids then k1 output ids (target first).  rows_s: (m + k1) rows
+// of ld elements.  e_s: m * k1 scaled errors (+ m * k1 raw errors in the
+// shared-C variant).  CREG: C lives in registers (k1 <= K1R); otherwise it is
+// read from shared memory and k1 <= 32.
+template <typename T, int NCH, bool CREG, int K1R>
+__device__ __forceinline__ void window_update(const ModelView<T> &mv, const int *ids_s, int m,
+                                              int k1, T alpha, bool exact, const T *sig_s,
+                                              bool want_loss, double &loss_acc,
+                                              long long &cell_acc, T *rows_s, T *e_s,
+                                              int lane) {
+  using V = typename Vec<T>::type;
+  constexpr int VN = Vec<T>::N;
+  const int64_t ld = mv.ld;
+  const int nvec = mv.nvec;
+  const int nrows = m + k1;
+
+  // 1. gather every row of the window before any scatter (snapshot semantics)
+  for (int r = 0; r < nrows; ++r) {
+    const int id = ids_s[r];
+    const T *src = (r < m ? mv.in_src : mv.out_src) + (int64_t)id * ld;
+    T *dst = rows_s + (int64_t)r * ld;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) cp_async16(dst + c * VN, src + c * VN);
+    }
+  }
+  cp_async_wait_all();
+  // each lane reads back only the chunks it copied itself: no warp barrier needed
+
+  if constexpr (CREG) {
+    constexpr int NV = (K1R <= 8) ? 8 : 16;
+    V c[K1R][NCH];
+#pragma unroll
+    for (int k = 0; k < K1R; ++k)
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        const int ch = lane + 32 * j;
+        c[k][j] = (k < k1 && ch < nvec)
+                      ? *reinterpret_cast<const V *>(rows_s + (int64_t)(m + k) * ld + ch * VN)
+                      : vzero(T());
+      }
+    const int my_k = reduced_index<NV>(lane);
+    const bool leader = (lane & ((32 / NV) - 1)) == 0;
+    for (int i = 0; i < m; ++i) {
+      V a[NCH];
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        const int ch = lane + 32 * j;
+        a[j] = ch < nvec ? *reinterpret_cast<const V *>(rows_s + (int64_t)i * ld + ch * VN)
+                         : vzero(T());
+      }
+      T p[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        T acc = T(0);
+        if (k < K1R) {
+#pragma unroll
+          for (int j = 0; j < NCH; ++j) acc += vdot(a[j], c[k < K1R ? k : 0][j]);
+        }
+        p[k] = acc;
+      }
+      const T s = transpose_reduce<NV>(p, lane);
+      T er = T(0), es = T(0);
+      if (my_k < k1) {
+        cell_error<T>(s, my_k, alpha, exact, sig_s, er, es);
+        if (leader) {
+          e_s[i * k1 + my_k] = es;
+          if (want_loss) {
+            loss_acc += softplus(my_k == 0 ? -(double)s : (double)s);
+            cell_acc += 1;
+          }
+        }
+      }
+      // dA_i = alpha * sum_k err_ik C_k  (alpha applied after the sum, :201-210)
+      V d[NCH];
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) d[j] = vzero(T());
+#pragma unroll
+      for (int k = 0; k < K1R; ++k) {
+        const T ek = __shfl_sync(0xffffffffu, er, group_leader<NV>(k));
+        if (k < k1) {
+#pragma unroll
+          for (int j = 0; j < NCH; ++j) vfma(d[j], ek, c[k][j]);
+        }
+      }
+      T *dst = mv.in_dst + (int64_t)ids_s[i] * ld;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        const int ch = lane + 32 * j;
+        if (ch < nvec) {
+          vscale(d[j], alpha);
+          red_add(dst + ch * VN, d[j]);
+        }
+      }
+    }
+    __syncwarp();
+    // dC_k = sum_i (alpha err_ik) A_i, one column chunk at a time
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int ch = lane + 32 * j;
+      V acc[K1R];
+#pragma unroll
+      for (int k = 0; k < K1R; ++k) acc[k] = vzero(T());
+      if (ch < nvec) {
+        for (int i = 0; i < m; ++i) {
+          const V a = *reinterpret_cast<const V *>(rows_s + (int64_t)i * ld + ch * VN);
+#pragma unroll
+          for (int k = 0; k < K1R; ++k)
+            if (k < k1) vfma(acc[k], e_s[i * k1 + k], a);
+        }
+#pragma unroll
+        for (int k = 0; k < K1R; ++k)
+          if (k < k1) red_add(mv.out_dst + (int64_t)ids_s[m + k] * ld + ch * VN, acc[k]);
+      }
+    }
+  } else {
+    // shared-memory C (k1 <= 32): scores, errors to smem, then dA and dC passes
+    constexpr int NV = 32;
+    T *er_s = e_s + m * k1;
+    const int my_k = reduced_index<NV>(lane);
+    for (int i = 0; i < m; ++i) {
+      V a[NCH];
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        const int ch = lane + 32 * j;
+        a[j] = ch < nvec ? *reinterpret_cast<const V *>(rows_s + (int64_t)i * ld + ch * VN)
+                         : vzero(T());
+      }
+      T p[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        T acc = T(0);
+        if (k < k1) {
+#pragma unroll
+          for (int j = 0; j < NCH; ++j) {
+            const int ch = lane + 32 * j;
+            if (ch < nvec)
+              acc += vdot(a[j], *reinterpret_cast<const V *>(rows_s + (int64_t)(m + k) * ld + ch * VN));
+          }
+        }
+        p[k] = acc;
+      }
+      const T s = transpose_reduce<NV>(p, lane);
+      if (my_k < k1) {
+        T er, es;
+        cell_error<T>(s, my_k, alpha, exact, sig_s, er, es);
+        e_s[i * k1 + my_k] = es;
+        er_s[i * k1 + my_k] = er;
+        if (want_loss) {
+          loss_acc += softplus(my_k == 0 ? -(double)s : (double)s);
+          cell_acc += 1;
+        }
+      }
+    }
+    __syncwarp();
+    for (int i = 0; i < m; ++i) {
+      T *dst = mv.in_dst + (int64_t)ids_s[i] * ld;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        const int ch = lane + 32 * j;
+        if (ch < nvec) {
+          V d = vzero(T());
+          for (int k = 0; k < k1; ++k)
+            vfma(d, er_s[i * k1 + k], *reinterpret_cast<const V *>(rows_s + (int64_t)(m + k) * ld + ch * VN));
+          vscale(d, alpha);
+          red_add(dst + ch * VN, d);
+        }
+      }
+    }
+    constexpr int KG = 8;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int ch = lane + 32 * j;
+      if (ch >= nvec) continue;
+      for (int k0 = 0; k0 < k1; k0 += KG) {
+        V acc[KG];
+#pragma unroll
+        for (int q = 0; q < KG; ++q) acc[q] = vzero(T());
+        for (int i = 0; i < m; ++i) {
+          const V a = *reinterpret_cast<const V *>(rows_s + (int64_t)i * ld + ch * VN);
+#pragma unroll
+          for (int q = 0; q < KG; ++q)
+            if (k0 + q < k1) vfma(acc[q], e_s[i * k1 + k0 + q], a);
+        }
+#pragma unroll
+        for (int q = 0; q < KG; ++q)
+          if (k0 + q < k1) red_add(mv.out_dst + (int64_t)ids_s[m + k0 + q] * ld + ch * VN, acc[q]);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+}  // namespace sgns

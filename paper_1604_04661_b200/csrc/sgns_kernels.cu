@@ -1,0 +1,793 @@
+// sgns_kernels.cu -- kernels and C ABI of the B200-native pSGNScc hot path.
+//
+// Kernels:
+//   update_windows_kernel  packed windows (process_batch / microbench), one warp per window
+//   drive_kernel           the fused, resumable epoch driver: one warp = one worker that
+//                          walks its contiguous sentence range (trainer.py:217-311)
+//   init_model_kernel      init_model (model.py:64-74), bit-identical
+//   expand_slots_kernel    the reference's negative slot table (corpus.py:139-155)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "../../include/sgns_b200.h"
+#include "sgns_device.cuh"
+
+namespace sgns {
+
+constexpr int kMaxSentence = 1024;
+constexpr int kMaxK1 = 32;
+
+__host__ __device__ inline int64_t round16(int64_t b) { return (b + 15) & ~int64_t(15); }
+
+// shared-memory slab of one warp
+struct Slab {
+  int64_t rows, e, ids, kept, off, total;
+};
+__host__ __device__ inline Slab slab_layout(int64_t elem, int64_t ld, int mcap, int k1, int kept_cap) {
+  Slab s;
+  s.rows = 0;
+  s.e = round16((int64_t)(mcap + k1) * ld * elem);
+  s.ids = s.e + round16((int64_t)2 * mcap * k1 * elem);
+  s.kept = s.ids + round16((int64_t)(mcap + k1) * 4);
+  s.off = s.kept + round16((int64_t)kept_cap * 4);
+  s.total = s.off + round16((int64_t)kept_cap * 4);
+  return s;
+}
+__host__ __device__ inline int64_t table_bytes(int64_t elem) { return round16(kSigBins * elem); }
+
+template <typename T>
+__device__ __forceinline__ void load_table(T *sig_s, const T *sig_g) {
+  for (int i = threadIdx.x; i < kSigBins; i += blockDim.x) sig_s[i] = sig_g[i];
+  __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ void flush_loss(double loss, long long cells, double *dst_loss,
+                                           int64_t *dst_cells, bool atomic, int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    loss += __shfl_xor_sync(0xffffffffu, loss, o);
+    cells += __shfl_xor_sync(0xffffffffu, cells, o);
+  }
+  if (lane == 0 && (cells != 0 || loss != 0.0)) {
+    if (atomic) {
+      atomicAdd(dst_loss, loss);
+      atomicAdd(reinterpret_cast<unsigned long long *>(dst_cells), (unsigned long long)cells);
+    } else {
+      *dst_loss += loss;
+      *dst_cells += cells;
+    }
+  }
+}
+
+// ------------------------------------------------------- update_windows ----
+template <typename T> struct UpdateArgs {
+  ModelView<T> mv;
+  const int32_t *in_off, *in_ids, *out_ids;
+  int n_win, k1, mcap;
+  const T *alpha, *sig;
+  int exact, loss_every;
+  double *loss_sum;
+  int64_t *loss_cells;
+  int32_t *error;
+  int wpb;
+};
+
+template <typename T, int NCH, bool CREG, int K1R>
+__global__ void __launch_bounds__(256) update_windows_kernel(UpdateArgs<T> p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  T *sig_s = reinterpret_cast<T *>(smem);
+  load_table(sig_s, p.sig);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Slab L = slab_layout(sizeof(T), p.mv.ld, p.mcap, p.k1, 0);
+  unsigned char *base = smem + table_bytes(sizeof(T)) + (int64_t)warp * L.total;
+  T *rows_s = reinterpret_cast<T *>(base + L.rows);
+  T *e_s = reinterpret_cast<T *>(base + L.e);
+  int *ids_s = reinterpret_cast<int *>(base + L.ids);
+  double loss = 0.0;
+  long long cells = 0;
+  for (int w = blockIdx.x * p.wpb + warp; w < p.n_win; w += gridDim.x * p.wpb) {
+    const int lo = p.in_off[w], hi = p.in_off[w + 1];
+    const int m = hi - lo;
+    if (m < 1 || m > p.mcap) {
+      if (lane == 0 && p.error) atomicExch(p.error, 1);
+      continue;
+    }
+    for (int r = lane; r < m + p.k1; r += 32)
+      ids_s[r] = r < m ? p.in_ids[lo + r] : p.out_ids[(int64_t)w * p.k1 + (r - m)];
+    __syncwarp();
+    const bool want = p.loss_every > 0 && (w % p.loss_every) == 0;
+    window_update<T, NCH, CREG, K1R>(p.mv, ids_s, m, p.k1, p.alpha[w], p.exact != 0, sig_s, want,
+                                     loss, cells, rows_s, e_s, lane);
+  }
+  if (p.loss_every > 0) flush_loss<T>(loss, cells, p.loss_sum, p.loss_cells, true, lane);
+}
+
+// ---------------------------------------------------------------- driver ----
+template <typename T> struct DriveArgs {
+  ModelView<T> mv;
+  const int32_t *ids;
+  const int64_t *offsets;
+  const double *keep;
+  const int32_t *slots;
+  uint64_t n_slots;
+  const uint32_t *alias_thr;
+  const int32_t *alias_idx;
+  uint32_t vocab;
+  uint32_t key0, key1;
+  int window, dynamic, k_neg, cap, exact;
+  const T *sig;
+  double alpha0, floor_frac, total_x_epochs;
+  int64_t refresh;
+  unsigned long long *shared;
+  int epochs, loss_every;
+  sgns_worker *workers;
+  int n_workers;
+  int64_t budget;
+  double *loss_by_epoch;
+  int64_t *cells_by_epoch;
+  int update;
+  int kept_cap;
+  int64_t trace_cap;
+  int32_t *trace;
+  double *trace_alpha;
+  int64_t *trace_count;
+  int32_t *error;
+  int wpb;
+};
+
+// Splitmix stream window: 32 consecutive draws evaluated by the 32 lanes.
+struct SmBatch {
+  uint64_t base;  // stream state before draw 0 of this batch
+  uint64_t z;     // this lane's draw
+  int used;       // draws consumed so far (uniform)
+  __device__ __forceinline__ void refill(uint64_t st, int lane) {
+    base = st;
+    z = sm_mix(st + (uint64_t)(lane + 1) * kGolden);
+    used = 0;
+  }
+  __device__ __forceinline__ uint64_t state_after() const { return base + (uint64_t)used * kGolden; }
+};
+
+template <typename T, int NCH, bool CREG, int K1R, int RNG>
+__global__ void __launch_bounds__(256) drive_kernel(DriveArgs<T> p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  T *sig_s = reinterpret_cast<T *>(smem);
+  load_table(sig_s, p.sig);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wid = blockIdx.x * p.wpb + warp;
+  if (wid >= p.n_workers) return;
+  const int k1 = p.k_neg + 1;
+  const int mcap = min(p.cap, 2 * p.window);
+  const Slab L = slab_layout(sizeof(T), p.mv.ld, mcap, k1, p.kept_cap);
+  unsigned char *base = smem + table_bytes(sizeof(T)) + (int64_t)warp * L.total;
+  T *rows_s = reinterpret_cast<T *>(base + L.rows);
+  T *e_s = reinterpret_cast<T *>(base + L.e);
+  int *ids_s = reinterpret_cast<int *>(base + L.ids);
+  int *kept_s = reinterpret_cast<int *>(base + L.kept);
+  int *koff_s = reinterpret_cast<int *>(base + L.off);
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  sgns_worker S = p.workers[wid];
+  if (S.done) return;
+  double alpha = S.alpha, read_local = S.read_local, trained_local = S.trained_local;
+  T alpha_t = (T)alpha;
+  uint64_t rng = S.rng;
+  int64_t s = S.next_sent, budget_used = 0, trained = 0, kc = S.kernel_counter;
+  int epoch = S.epoch;
+  int done = 0;
+  double loss = 0.0;
+  long long cells = 0;
+  const int rec_len = 4 + p.cap + k1;
+
+  auto close_epoch = [&]() {
+    flush_loss<T>(loss, cells, p.loss_by_epoch + (int64_t)wid * p.epochs + epoch,
+                  p.cells_by_epoch + (int64_t)wid * p.epochs + epoch, false, lane);
+    loss = 0.0;
+    cells = 0;
+    epoch += 1;
+    s = S.lo;
+    if (epoch >= p.epochs) {
+      done = 1;
+      if (lane == 0) {  // ThreadRun.flush_counters (trainer.py:448-453)
+        atomicAdd(p.shared, (unsigned long long)(int64_t)read_local);
+        atomicAdd(p.shared + 1, (unsigned long long)(int64_t)trained_local);
+      }
+      read_local = trained_local = 0.0;
+    }
+  };
+
+  while (!done && budget_used < p.budget) {
+    if (s >= S.hi) {
+      close_epoch();
+      continue;
+    }
+    const int64_t lo_t = p.offsets[s], hi_t = p.offsets[s + 1];
+    const int n = (int)(hi_t - lo_t);
+    if (n > p.kept_cap) {
+      if (lane == 0 && p.error) atomicExch(p.error, 2);
+      done = 1;
+      break;
+    }
+    read_local += (double)n;
+    budget_used += n;
+    if (read_local >= (double)p.refresh) {  // alpha refresh (trainer.py:243-252)
+      unsigned long long before = 0;
+      if (lane == 0) {
+        before = atomicAdd(p.shared, (unsigned long long)(int64_t)read_local);
+        atomicAdd(p.shared + 1, (unsigned long long)(int64_t)trained_local);
+      }
+      before = __shfl_sync(0xffffffffu, before, 0);
+      const double now = (double)(int64_t)(before + (unsigned long long)(int64_t)read_local);
+      read_local = trained_local = 0.0;
+      double frac = 1.0 - now / (p.total_x_epochs + 1.0);
+      if (frac < p.floor_frac) frac = p.floor_frac;
+      alpha = p.alpha0 * frac;
+      alpha_t = (T)alpha;
+    }
+    // subsample (corpus.py:168-181): one uniform per token, survivors compacted in order
+    int nk = 0;
+    for (int b0 = 0; b0 < n; b0 += 32) {
+      const int i = b0 + lane;
+      const bool valid = i < n;
+      const int w = valid ? p.ids[lo_t + i] : 0;
+      bool keep = valid;
+      if (p.keep != nullptr && valid) {
+        double u;
+        if (RNG == SGNS_RNG_SPLITMIX) {
+          u = u53(sm_mix(rng + (uint64_t)(i + 1) * kGolden));
+        } else {
+          const uint4 o = philox_tok((uint64_t)(lo_t + i), (uint32_t)epoch, kTagSub, p.key0, p.key1);
+          u = u53((uint64_t)o.x | ((uint64_t)o.y << 32));
+        }
+        keep = u < p.keep[w];
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int pos = nk + __popc(mask & lt_mask);
+        kept_s[pos] = w;
+        koff_s[pos] = i;
+      }
+      nk += __popc(mask);
+    }
+    if (RNG == SGNS_RNG_SPLITMIX && p.keep != nullptr) rng += (uint64_t)n * kGolden;
+    __syncwarp();
+
+    SmBatch sb;
+    for (int pos = 0; pos < nk; ++pos) {
+      int b = p.window;
+      if (RNG == SGNS_RNG_SPLITMIX) {
+        sb.refill(rng, lane);
+        if (p.dynamic) {
+          const uint64_t bz = __shfl_sync(0xffffffffu, sb.z, 0);
+          b = 1 + (int)(bz % (uint64_t)p.window);
+          sb.used = 1;
+        }
+      } else if (p.dynamic) {
+        const uint4 o = philox_tok((uint64_t)(lo_t + koff_s[pos]), (uint32_t)epoch, kTagWin, p.key0, p.key1);
+        b = 1 + (int)(((uint64_t)o.x * (uint64_t)p.window) >> 32);
+      }
+      const int wlo = max(pos - b, 0);
+      const int whi = min(pos + b + 1, nk);
+      const int m = whi - wlo - 1;
+      if (m <= 0) {
+        if (RNG == SGNS_RNG_SPLITMIX) rng = sb.state_after();
+        continue;
+      }
+      const int target = kept_s[pos];
+      const int left = pos - wlo;
+      uint32_t attempt = 0;  // philox attempt counter within the chunk
+      int chunk = 0;
+      for (int start = 0; start < m; start += p.cap, ++chunk) {
+        const int mc = min(p.cap, m - start);
+        for (int r = lane; r < mc; r += 32) {
+          const int q = start + r;
+          ids_s[r] = q < left ? kept_s[wlo + q] : kept_s[pos + 1 + (q - left)];
+        }
+        if (lane == 0) ids_s[mc] = target;
+        // K shared negatives, rejecting the target (kernel_batched.py:57-66)
+        int need = p.k_neg;
+        attempt = 0;
+        while (need > 0) {
+          bool ok = false;
+          int word = -1;
+          int span;
+          if (RNG == SGNS_RNG_SPLITMIX) {
+            if (sb.used >= 32) sb.refill(sb.state_after(), lane);
+            span = min(32 - sb.used, need + 2);
+            if (lane >= sb.used && lane < sb.used + span) {
+              word = p.slots[sb.z % p.n_slots];
+              ok = word != target;
+            }
+          } else {
+            span = min(32, need + 2);
+            if (lane < span) {
+              const uint32_t a = attempt + (uint32_t)lane;
+              const uint4 o = philox_tok((uint64_t)(lo_t + koff_s[pos]), (uint32_t)epoch,
+                                         kTagNeg | ((uint32_t)(chunk & 0xFF) << 16) | ((a >> 1) & 0xFFFFu),
+                                         p.key0, p.key1);
+              const uint32_t bw = (a & 1) ? o.z : o.x, coin = (a & 1) ? o.w : o.y;
+              const uint32_t bucket = (uint32_t)(((uint64_t)bw * (uint64_t)p.vocab) >> 32);
+              word = coin < p.alias_thr[bucket] ? (int)bucket : p.alias_idx[bucket];
+              ok = word != target;
+            }
+          }
+          const unsigned mask = __ballot_sync(0xffffffffu, ok);
+          const int avail = __popc(mask);
+          const int take = min(avail, need);
+          const int rank = __popc(mask & lt_mask);
+          if (ok && rank < take) ids_s[mc + 1 + (p.k_neg - need) + rank] = word;
+          int consumed_to;  // lane index one past the last consumed draw
+          if (take == need && take > 0) {
+            unsigned mm = mask;
+            for (int t = 1; t < take; ++t) mm &= mm - 1;  // drop take-1 lowest set bits
+            consumed_to = __ffs(mm);                      // 1-based lane of the take-th accept
+          } else {
+            consumed_to = (RNG == SGNS_RNG_SPLITMIX ? sb.used : 0) + span;
+          }
+          if (RNG == SGNS_RNG_SPLITMIX) sb.used = consumed_to;
+          else attempt += (uint32_t)consumed_to;
+          need -= take;
+        }
+        __syncwarp();
+        kc += 1;
+        const bool want = p.loss_every > 0 && (kc % p.loss_every) == 0;
+        if (p.trace_cap > 0) {
+          int64_t idx = p.trace_count[wid];
+          if (idx < p.trace_cap) {
+            int32_t *rec = p.trace + ((int64_t)wid * p.trace_cap + idx) * rec_len;
+            for (int r = lane; r < rec_len; r += 32) {
+              int v;
+              if (r == 0) v = target;
+              else if (r == 1) v = mc;
+              else if (r == 2) v = (int)s;
+              else if (r == 3) v = epoch;
+              else if (r < 4 + p.cap) v = (r - 4) < mc ? ids_s[r - 4] : -1;
+              else v = ids_s[mc + (r - 4 - p.cap)];
+              rec[r] = v;
+            }
+            if (lane == 0) p.trace_alpha[(int64_t)wid * p.trace_cap + idx] = (double)alpha_t;
+          }
+          __syncwarp();
+          if (lane == 0) p.trace_count[wid] = idx + 1;
+        }
+        if (p.update)
+          window_update<T, NCH, CREG, K1R>(p.mv, ids_s, mc, k1, alpha_t, p.exact != 0, sig_s, want,
+                                           loss, cells, rows_s, e_s, lane);
+        __syncwarp();
+      }
+      if (RNG == SGNS_RNG_SPLITMIX) rng = sb.state_after();
+    }
+    trained += nk;
+    trained_local += (double)nk;
+    s += 1;
+  }
+  if (!done && s >= S.hi) close_epoch();  // ThreadRun.advance :435-441
+  if (!done || epoch < p.epochs) {
+    flush_loss<T>(loss, cells, p.loss_by_epoch + (int64_t)wid * p.epochs + min(epoch, p.epochs - 1),
+                  p.cells_by_epoch + (int64_t)wid * p.epochs + min(epoch, p.epochs - 1), false, lane);
+  }
+  if (lane == 0) {
+    sgns_worker &o = p.workers[wid];
+    o.next_sent = s;
+    o.epoch = epoch;
+    o.done = done;
+    o.rng = rng;
+    o.alpha = alpha;
+    o.read_local = read_local;
+    o.trained_local = trained_local;
+    o.kernel_counter = kc;
+    o.words_read = S.words_read + budget_used;
+    o.words_trained = S.words_trained + trained;
+  }
+}
+
+// ------------------------------------------------------------------ init ----
+template <typename T>
+__global__ void init_model_kernel(T *m_in, T *m_out, int64_t V, int dim, int64_t ld, uint64_t s0) {
+  const double bound = 0.5 / dim;
+  const int64_t total = V * ld;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / ld;
+    const int col = (int)(e - row * ld);
+    T v = T(0);
+    if (col < dim) {
+      const uint64_t n = (uint64_t)(row * dim + col);  // draw index in model.py's row-major fill
+      const double u = u53(sm_mix(s0 + (n + 1) * kGolden));
+      v = (T)((u * 2.0 - 1.0) * bound);
+    }
+    m_in[e] = v;
+    m_out[e] = T(0);
+  }
+}
+
+__global__ void expand_slots_kernel(const int64_t *bounds, int64_t V, int32_t *slots, int64_t n) {
+  for (int64_t sidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sidx < n;
+       sidx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = V - 1;  // first w with bounds[w] > sidx
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (bounds[mid] > sidx) hi = mid;
+      else lo = mid + 1;
+    }
+    slots[sidx] = (int32_t)lo;
+  }
+}
+
+// ----------------------------------------------------------- dispatching ----
+static int nch_for(int nvec) {
+  const int need = (nvec + 31) / 32;
+  if (need <= 1) return 1;
+  if (need <= 2) return 2;
+  if (need <= 3) return 3;
+  if (need <= 4) return 4;
+  if (need <= 8) return 8;
+  return -1;
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <typename K>
+static int prepare(K kernel, int64_t smem_bytes) {
+  if (smem_bytes > 227 * 1024) return SGNS_E_SMEM;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_bytes);
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+// Choose warps per block maximising resident warps for a given per-warp slab.
+template <typename K>
+static int choose_wpb(K kernel, int64_t table, int64_t slab, int *wpb_out, int *blocks_per_sm) {
+  int best = -1, best_w = 1, best_b = 1;
+  for (int w : {1, 2, 4, 8}) {
+    const int64_t bytes = table + (int64_t)w * slab;
+    if (bytes > 227 * 1024) break;
+    if (prepare(kernel, bytes) != 0) break;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, w * 32, (size_t)bytes) != cudaSuccess)
+      break;
+    if (nb * w > best) {
+      best = nb * w;
+      best_w = w;
+      best_b = nb;
+    }
+  }
+  if (best <= 0) return SGNS_E_SMEM;
+  *wpb_out = best_w;
+  *blocks_per_sm = best_b;
+  return 0;
+}
+
+template <typename T, int NCH, bool CREG, int K1R>
+static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
+  auto kern = update_windows_kernel<T, NCH, CREG, K1R>;
+  const Slab L = slab_layout(sizeof(T), a.mv.ld, a.mcap, a.k1, 0);
+  int wpb = 0, bps = 0;
+  int rc = choose_wpb(kern, table_bytes(sizeof(T)), L.total, &wpb, &bps);
+  if (rc) return rc;
+  a.wpb = wpb;
+  const int64_t bytes = table_bytes(sizeof(T)) + (int64_t)wpb * L.total;
+  const int64_t blocks_needed = (a.n_win + wpb - 1) / wpb;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)num_sms() * bps));
+  kern<<<grid, wpb * 32, bytes, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+template <typename T, int NCH, bool CREG, int K1R, int RNG>
+static int launch_drive_t(DriveArgs<T> a, int wpb_req, cudaStream_t st) {
+  auto kern = drive_kernel<T, NCH, CREG, K1R, RNG>;
+  const int k1 = a.k_neg + 1;
+  const Slab L = slab_layout(sizeof(T), a.mv.ld, std::min(a.cap, 2 * a.window), k1, a.kept_cap);
+  int wpb = 0, bps = 0;
+  int rc = choose_wpb(kern, table_bytes(sizeof(T)), L.total, &wpb, &bps);
+  if (rc) return rc;
+  if (wpb_req > 0) wpb = wpb_req;
+  a.wpb = wpb;
+  const int64_t bytes = table_bytes(sizeof(T)) + (int64_t)wpb * L.total;
+  if ((rc = prepare(kern, bytes))) return rc;
+  const int grid = (a.n_workers + wpb - 1) / wpb;
+  kern<<<grid, wpb * 32, bytes, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+template <typename T, int NCH>
+static int dispatch_update(UpdateArgs<T> a, cudaStream_t st) {
+  if constexpr (sizeof(T) == 4 && NCH <= 4) {
+    if (a.k1 <= 6) return launch_update_t<T, NCH, true, 6>(a, st);
+  }
+  if constexpr (sizeof(T) == 4 && NCH <= 3) {
+    if (a.k1 <= 8) return launch_update_t<T, NCH, true, 8>(a, st);
+  }
+  return launch_update_t<T, NCH, false, 0>(a, st);
+}
+
+template <typename T, int NCH, int RNG>
+static int dispatch_drive(DriveArgs<T> a, int wpb, cudaStream_t st) {
+  const int k1 = a.k_neg + 1;
+  if constexpr (sizeof(T) == 4 && NCH <= 4) {
+    if (k1 <= 6) return launch_drive_t<T, NCH, true, 6, RNG>(a, wpb, st);
+  }
+  if constexpr (sizeof(T) == 4 && NCH <= 3) {
+    if (k1 <= 8) return launch_drive_t<T, NCH, true, 8, RNG>(a, wpb, st);
+  }
+  return launch_drive_t<T, NCH, false, 0, RNG>(a, wpb, st);
+}
+
+template <typename T>
+static int update_typed(UpdateArgs<T> a, int nch, cudaStream_t st) {
+  switch (nch) {
+    case 1: return dispatch_update<T, 1>(a, st);
+    case 2: return dispatch_update<T, 2>(a, st);
+    case 3: return dispatch_update<T, 3>(a, st);
+    case 4: return dispatch_update<T, 4>(a, st);
+    case 8: return dispatch_update<T, 8>(a, st);
+  }
+  return SGNS_E_SHAPE;
+}
+
+template <typename T, int RNG>
+static int drive_typed_rng(DriveArgs<T> a, int nch, int wpb, cudaStream_t st) {
+  switch (nch) {
+    case 1: return dispatch_drive<T, 1, RNG>(a, wpb, st);
+    case 2: return dispatch_drive<T, 2, RNG>(a, wpb, st);
+    case 3: return dispatch_drive<T, 3, RNG>(a, wpb, st);
+    case 4: return dispatch_drive<T, 4, RNG>(a, wpb, st);
+    case 8: return dispatch_drive<T, 8, RNG>(a, wpb, st);
+  }
+  return SGNS_E_SHAPE;
+}
+
+template <typename T>
+static int drive_typed(const sgns_drive_params *p, cudaStream_t st) {
+  DriveArgs<T> a;
+  std::memset(&a, 0, sizeof(a));
+  T *mi = static_cast<T *>(p->d_m_in), *mo = static_cast<T *>(p->d_m_out);
+  a.mv = ModelView<T>{mi, mo, mi, mo, p->ld, (int)(p->ld * (int64_t)sizeof(T) / 16)};
+  a.ids = p->d_ids;
+  a.offsets = p->d_offsets;
+  a.keep = p->d_keep_probs;
+  a.slots = p->d_slots;
+  a.n_slots = (uint64_t)p->n_slots;
+  a.alias_thr = p->d_alias_thr;
+  a.alias_idx = p->d_alias_idx;
+  a.vocab = (uint32_t)p->vocab;
+  a.key0 = (uint32_t)p->seed;
+  a.key1 = (uint32_t)(p->seed >> 32);
+  a.window = p->window;
+  a.dynamic = p->dynamic;
+  a.k_neg = p->k_neg;
+  a.cap = p->batch_cap;
+  a.exact = p->sigmoid_mode == SGNS_SIGMOID_EXACT;
+  a.sig = static_cast<const T *>(p->d_sig_table);
+  a.alpha0 = p->alpha0;
+  a.floor_frac = p->floor_frac;
+  a.total_x_epochs = p->total_x_epochs;
+  a.refresh = p->refresh_words;
+  a.shared = reinterpret_cast<unsigned long long *>(p->d_shared);
+  a.epochs = p->epochs;
+  a.loss_every = p->loss_every;
+  a.workers = p->d_workers;
+  a.n_workers = p->n_workers;
+  a.budget = p->word_budget;
+  a.loss_by_epoch = p->d_loss_by_epoch;
+  a.cells_by_epoch = p->d_cells_by_epoch;
+  a.update = p->update;
+  a.kept_cap = ((std::max(p->max_sentence, 1) + 31) / 32) * 32;
+  a.trace_cap = p->trace_cap;
+  a.trace = p->d_trace;
+  a.trace_alpha = p->d_trace_alpha;
+  a.trace_count = p->d_trace_count;
+  a.error = p->d_error;
+  const int nch = nch_for(a.mv.nvec);
+  if (nch < 0) return SGNS_E_SHAPE;
+  if (p->rng_mode == SGNS_RNG_SPLITMIX) return drive_typed_rng<T, SGNS_RNG_SPLITMIX>(a, nch, p->warps_per_block, st);
+  return drive_typed_rng<T, SGNS_RNG_PHILOX>(a, nch, p->warps_per_block, st);
+}
+
+static bool ld_ok(int32_t dtype, int32_t dim, int64_t ld) {
+  const int64_t elem = dtype == SGNS_F64 ? 8 : 4;
+  return dim >= 1 && ld >= dim && (ld * elem) % 16 == 0;
+}
+
+}  // namespace sgns
+
+using namespace sgns;
+
+extern "C" {
+
+int sgns_abi_version(void) { return SGNS_ABI_VERSION; }
+
+const char *sgns_error_string(int32_t code) {
+  switch (code) {
+    case SGNS_OK: return "ok";
+    case SGNS_E_ARG: return "invalid argument";
+    case SGNS_E_SHAPE: return "shape outside the supported envelope (dim <= 1024 f32 / 512 f64, k+1 <= 32)";
+    case SGNS_E_SMEM: return "per-warp staging does not fit in 227 KB of shared memory";
+    case SGNS_E_DEVICE: return "device-side validation failed";
+  }
+  if (code > 0) return cudaGetErrorString((cudaError_t)code);
+  return "unknown error";
+}
+
+int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, const void *d_m_in_src,
+                        const void *d_m_out_src, int64_t vocab, int32_t dim, int64_t ld,
+                        const int32_t *d_in_off, const int32_t *d_in_ids, const int32_t *d_out_ids,
+                        int32_t n_windows, int32_t k1, int32_t max_inputs, const void *d_alpha,
+                        const void *d_sig_table, int32_t sigmoid_mode, int32_t loss_every,
+                        double *d_loss_sum, int64_t *d_loss_cells, int32_t *d_error, void *stream) {
+  if (!d_m_in_dst || !d_m_out_dst || !d_m_in_src || !d_m_out_src || !d_in_off || !d_in_ids ||
+      !d_out_ids || !d_alpha || !d_sig_table || vocab < 1)
+    return SGNS_E_ARG;
+  if (n_windows == 0) return SGNS_OK;
+  if (n_windows < 0 || max_inputs < 1 || k1 < 2 || k1 > kMaxK1 || !ld_ok(dtype, dim, ld))
+    return SGNS_E_SHAPE;
+  if (loss_every > 0 && (!d_loss_sum || !d_loss_cells)) return SGNS_E_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == SGNS_F32) {
+    UpdateArgs<float> a;
+    a.mv = ModelView<float>{static_cast<float *>(d_m_in_dst), static_cast<float *>(d_m_out_dst),
+                            static_cast<const float *>(d_m_in_src), static_cast<const float *>(d_m_out_src),
+                            ld, (int)(ld / 4)};
+    a.in_off = d_in_off; a.in_ids = d_in_ids; a.out_ids = d_out_ids;
+    a.n_win = n_windows; a.k1 = k1; a.mcap = max_inputs;
+    a.alpha = static_cast<const float *>(d_alpha);
+    a.sig = static_cast<const float *>(d_sig_table);
+    a.exact = sigmoid_mode == SGNS_SIGMOID_EXACT;
+    a.loss_every = loss_every; a.loss_sum = d_loss_sum; a.loss_cells = d_loss_cells;
+    a.error = d_error; a.wpb = 1;
+    return update_typed<float>(a, nch_for(a.mv.nvec), st);
+  }
+  if (dtype == SGNS_F64) {
+    UpdateArgs<double> a;
+    a.mv = ModelView<double>{static_cast<double *>(d_m_in_dst), static_cast<double *>(d_m_out_dst),
+                             static_cast<const double *>(d_m_in_src),
+                             static_cast<const double *>(d_m_out_src), ld, (int)(ld / 2)};
+    a.in_off = d_in_off; a.in_ids = d_in_ids; a.out_ids = d_out_ids;
+    a.n_win = n_windows; a.k1 = k1; a.mcap = max_inputs;
+    a.alpha = static_cast<const double *>(d_alpha);
+    a.sig = static_cast<const double *>(d_sig_table);
+    a.exact = sigmoid_mode == SGNS_SIGMOID_EXACT;
+    a.loss_every = loss_every; a.loss_sum = d_loss_sum; a.loss_cells = d_loss_cells;
+    a.error = d_error; a.wpb = 1;
+    return update_typed<double>(a, nch_for(a.mv.nvec), st);
+  }
+  return SGNS_E_ARG;
+}
+
+int sgns_drive(const sgns_drive_params *p, void *stream) {
+  if (!p || !p->d_m_in || !p->d_m_out || !p->d_ids || !p->d_offsets || !p->d_sig_table ||
+      !p->d_shared || !p->d_workers || !p->d_loss_by_epoch || !p->d_cells_by_epoch)
+    return SGNS_E_ARG;
+  if (p->n_workers <= 0) return SGNS_OK;
+  if (p->k_neg < 1 || p->k_neg + 1 > kMaxK1 || p->window < 1 || p->batch_cap < 1 ||
+      p->epochs < 1 || !ld_ok(p->dtype, p->dim, p->ld) || p->max_sentence > kMaxSentence ||
+      p->vocab < 2)
+    return SGNS_E_SHAPE;
+  if (p->rng_mode == SGNS_RNG_SPLITMIX && (!p->d_slots || p->n_slots < 1)) return SGNS_E_ARG;
+  if (p->rng_mode == SGNS_RNG_PHILOX && (!p->d_alias_thr || !p->d_alias_idx)) return SGNS_E_ARG;
+  if (p->rng_mode != SGNS_RNG_SPLITMIX && p->rng_mode != SGNS_RNG_PHILOX) return SGNS_E_ARG;
+  if (p->trace_cap > 0 && (!p->d_trace || !p->d_trace_alpha || !p->d_trace_count)) return SGNS_E_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (p->dtype == SGNS_F32) return drive_typed<float>(p, st);
+  if (p->dtype == SGNS_F64) return drive_typed<double>(p, st);
+  return SGNS_E_ARG;
+}
+
+int sgns_init_model(int32_t dtype, void *d_m_in, void *d_m_out, int64_t vocab, int32_t dim,
+                    int64_t ld, uint64_t seed, void *stream) {
+  if (!d_m_in || !d_m_out || vocab < 1) return SGNS_E_ARG;
+  if (!ld_ok(dtype, dim, ld)) return SGNS_E_SHAPE;
+  // new_state(seed, 0x1017) (rng.py:50-56)
+  uint64_t z = seed ^ (0x1017ULL * kGolden + 1ULL);
+  z = (z ^ (z >> 30)) * kMix1;
+  z = (z ^ (z >> 27)) * kMix2;
+  const uint64_t s0 = z ^ (z >> 31);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t total = vocab * ld;
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 32);
+  if (dtype == SGNS_F32)
+    init_model_kernel<float><<<grid, 256, 0, st>>>(static_cast<float *>(d_m_in), static_cast<float *>(d_m_out),
+                                                     vocab, dim, ld, s0);
+  else if (dtype == SGNS_F64)
+    init_model_kernel<double><<<grid, 256, 0, st>>>(static_cast<double *>(d_m_in), static_cast<double *>(d_m_out),
+                                                      vocab, dim, ld, s0);
+  else
+    return SGNS_E_ARG;
+  return (int)cudaGetLastError();
+}
+
+int sgns_expand_slots(const int64_t *d_boundaries, int64_t vocab, int32_t *d_slots, int64_t n_slots,
+                      void *stream) {
+  if (!d_boundaries || !d_slots || vocab < 1 || n_slots < vocab) return SGNS_E_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = (int)std::min<int64_t>((n_slots + 255) / 256, (int64_t)num_sms() * 32);
+  expand_slots_kernel<<<grid, 256, 0, st>>>(d_boundaries, vocab, d_slots, n_slots);
+  return (int)cudaGetLastError();
+}
+
+int sgns_resident_workers(int32_t dtype, int32_t dim, int32_t window, int32_t k_neg, int32_t batch_cap,
+                          int32_t max_sentence, int32_t *out_workers) {
+  if (!out_workers) return SGNS_E_ARG;
+  const int64_t elem = dtype == SGNS_F64 ? 8 : 4;
+  const int64_t ld = ((dim * elem + 15) / 16) * 16 / elem;
+  const int nch = nch_for((int)(ld * elem / 16));
+  if (nch < 0 || k_neg + 1 > kMaxK1) return SGNS_E_SHAPE;
+  const int k1 = k_neg + 1;
+  const int kept = ((std::max(max_sentence, 1) + 31) / 32) * 32;
+  const Slab L = slab_layout(elem, ld, std::min(batch_cap, 2 * window), k1, kept);
+  int wpb = 0, bps = 0, rc;
+  // occupancy of the kernel this configuration dispatches to (registers + smem)
+  if (dtype == SGNS_F32 && nch <= 4 && k1 <= 6) {
+    switch (nch) {
+      case 1: rc = choose_wpb(drive_kernel<float, 1, true, 6, SGNS_RNG_PHILOX>, table_bytes(elem), L.total, &wpb, &bps); break;
+      case 2: rc = choose_wpb(drive_kernel<float, 2, true, 6, SGNS_RNG_PHILOX>, table_bytes(elem), L.total, &wpb, &bps); break;
+      case 3: rc = choose_wpb(drive_kernel<float, 3, true, 6, SGNS_RNG_PHILOX>, table_bytes(elem), L.total, &wpb, &bps); break;
+      default: rc = choose_wpb(drive_kernel<float, 4, true, 6, SGNS_RNG_PHILOX>, table_bytes(elem), L.total, &wpb, &bps); break;
+    }
+  } else if (dtype == SGNS_F32) {
+    rc = choose_wpb(drive_kernel<float, 8, false, 0, SGNS_RNG_PHILOX>, table_bytes(elem), L.total, &wpb, &bps);
+  } else {
+    rc = choose_wpb(drive_kernel<double, 8, false, 0, SGNS_RNG_PHILOX>, table_bytes(elem), L.total, &wpb, &bps);
+  }
+  if (rc) return rc;
+  *out_workers = wpb * bps * num_sms();
+  return SGNS_OK;
+}
+
+// Vose's alias method in float64 over count^power (host).
+int sgns_build_alias(const int64_t *h_counts, int64_t vocab, double power, uint32_t *h_thr,
+                     int32_t *h_alias) {
+  if (!h_counts || !h_thr || !h_alias || vocab < 1 || vocab > (int64_t)INT32_MAX) return SGNS_E_ARG;
+  std::vector<double> p(vocab);
+  double total = 0.0;
+  for (int64_t i = 0; i < vocab; ++i) {
+    if (h_counts[i] < 0) return SGNS_E_ARG;
+    p[i] = std::pow((double)h_counts[i], power);
+    total += p[i];
+  }
+  if (!(total > 0.0)) return SGNS_E_ARG;
+  std::vector<int32_t> small, large;
+  small.reserve(vocab);
+  large.reserve(vocab);
+  for (int64_t i = 0; i < vocab; ++i) {
+    p[i] = p[i] * (double)vocab / total;
+    (p[i] < 1.0 ? small : large).push_back((int32_t)i);
+  }
+  auto thr_of = [](double q) -> uint32_t {
+    if (q >= 1.0) return 0xFFFFFFFFu;
+    if (q <= 0.0) return 0u;
+    return (uint32_t)std::floor(std::ldexp(q, 32));
+  };
+  while (!small.empty() && !large.empty()) {
+    const int32_t s = small.back();
+    small.pop_back();
+    const int32_t l = large.back();
+    h_thr[s] = thr_of(p[s]);
+    h_alias[s] = l;
+    p[l] = (p[l] + p[s]) - 1.0;
+    if (p[l] < 1.0) {
+      large.pop_back();
+      small.push_back(l);
+    }
+  }
+  for (int32_t i : large) { h_thr[i] = 0xFFFFFFFFu; h_alias[i] = i; }
+  for (int32_t i : small) { h_thr[i] = 0xFFFFFFFFu; h_alias[i] = i; }  // rounding leftovers
+  return SGNS_OK;
+}
+
+}  // extern "C"

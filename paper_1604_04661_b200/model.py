@@ -1,0 +1,179 @@
+"""Model parameters: host `EmbeddingModel` (reference API) and its HBM twin `DeviceModel`.
+
+Reference map:
+  EmbeddingModel            sgns/model.py:29-53
+  init_model                sgns/model.py:64-74   (here: sgns_init_model on device, bit-identical)
+  sigmoid / sigmoid table   sgns/model.py:77-115  (host table uploaded; index math stays float64)
+
+HBM layout: each matrix is a (V, ld) row-major tensor with ld = dim rounded up
+so a row is a whole number of 16-byte chunks (ld == dim for dim % 4 == 0 in
+float32, e.g. 100/200/300); padding columns are zero and stay zero.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+SIGMOID_RANGE = 6.0
+SIGMOID_BINS = 1000
+
+
+@dataclass
+class EmbeddingModel:
+    input_vectors: np.ndarray  # V x D
+    output_vectors: np.ndarray  # V x D
+
+    @property
+    def vocab_size(self) -> int:
+        return self.input_vectors.shape[0]
+
+    @property
+    def dim(self) -> int:
+        return self.input_vectors.shape[1]
+
+    @property
+    def dtype(self) -> np.dtype:
+        return self.input_vectors.dtype
+
+    def copy(self) -> "EmbeddingModel":
+        return EmbeddingModel(self.input_vectors.copy(), self.output_vectors.copy())
+
+    def assert_finite(self) -> None:
+        if not np.isfinite(self.input_vectors).all():
+            raise FloatingPointError("non-finite entries in input_vectors")
+        if not np.isfinite(self.output_vectors).all():
+            raise FloatingPointError("non-finite entries in output_vectors")
+
+
+def sigmoid(x):
+    """Exact, numerically stable logistic function (scalar or array)."""
+    if np.isscalar(x) or np.ndim(x) == 0:
+        x = float(x)
+        if x >= 0:
+            return 1.0 / (1.0 + math.exp(-x))
+        ex = math.exp(x)
+        return ex / (1.0 + ex)
+    x = np.asarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    pos = x >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-x[pos]))
+    ex = np.exp(x[~pos])
+    out[~pos] = ex / (1.0 + ex)
+    return out
+
+
+def build_sigmoid_table(dtype=np.float32) -> np.ndarray:
+    """Left-edge sigmoid over [-6, 6) in 1000 bins (host float64, cast once)."""
+    edges = -SIGMOID_RANGE + np.arange(SIGMOID_BINS) * (2.0 * SIGMOID_RANGE / SIGMOID_BINS)
+    return sigmoid(edges).astype(dtype)
+
+
+SIGMOID_TABLE_F32 = build_sigmoid_table(np.float32)
+SIGMOID_TABLE_F64 = build_sigmoid_table(np.float64)
+
+
+def padded_ld(dim: int, dtype) -> int:
+    per16 = 16 // np.dtype(dtype).itemsize
+    return -(-dim // per16) * per16
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1604_04661_b200 needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def _tdtype(torch, dtype):
+    return torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
+
+
+def _cdtype(dtype) -> int:
+    return _lib.SGNS_F64 if np.dtype(dtype) == np.float64 else _lib.SGNS_F32
+
+
+def current_stream_ptr(device=None) -> int:
+    torch = _torch()
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class DeviceModel:
+    """M_in / M_out resident in HBM as (V, ld) tensors."""
+
+    def __init__(self, m_in, m_out, dim: int):
+        self.m_in = m_in
+        self.m_out = m_out
+        self.dim = dim
+
+    @property
+    def vocab_size(self) -> int:
+        return self.m_in.shape[0]
+
+    @property
+    def ld(self) -> int:
+        return self.m_in.shape[1]
+
+    @property
+    def np_dtype(self):
+        import torch
+        return np.float64 if self.m_in.dtype == torch.float64 else np.float32
+
+    @property
+    def cdtype(self) -> int:
+        return _cdtype(self.np_dtype)
+
+    @classmethod
+    def empty(cls, vocab_size: int, dim: int, dtype=np.float32, device="cuda") -> "DeviceModel":
+        torch = _torch()
+        ld = padded_ld(dim, dtype)
+        td = _tdtype(torch, dtype)
+        return cls(torch.zeros((vocab_size, ld), dtype=td, device=device),
+                   torch.zeros((vocab_size, ld), dtype=td, device=device), dim)
+
+    @classmethod
+    def from_host(cls, model: EmbeddingModel, device="cuda") -> "DeviceModel":
+        torch = _torch()
+        dm = cls.empty(model.vocab_size, model.dim, model.dtype, device)
+        dm.m_in[:, :model.dim].copy_(torch.from_numpy(np.ascontiguousarray(model.input_vectors)))
+        dm.m_out[:, :model.dim].copy_(torch.from_numpy(np.ascontiguousarray(model.output_vectors)))
+        return dm
+
+    def to_host(self) -> EmbeddingModel:
+        return EmbeddingModel(self.m_in[:, :self.dim].cpu().numpy().copy(),
+                              self.m_out[:, :self.dim].cpu().numpy().copy())
+
+    def copy_to_host(self, model: EmbeddingModel) -> None:
+        model.input_vectors[...] = self.m_in[:, :self.dim].cpu().numpy()
+        model.output_vectors[...] = self.m_out[:, :self.dim].cpu().numpy()
+
+    def clone(self) -> "DeviceModel":
+        return DeviceModel(self.m_in.clone(), self.m_out.clone(), self.dim)
+
+
+def init_device_model(vocab_size: int, dim: int, seed: int, dtype=np.float32,
+                      device="cuda") -> DeviceModel:
+    """init_model on device: U(-0.5/D, 0.5/D) from splitmix stream (seed, 0x1017), M_out = 0."""
+    if vocab_size < 1 or dim < 1:
+        raise ValueError("vocab_size and dim must be positive")
+    dm = DeviceModel.empty(vocab_size, dim, dtype, device)
+    rc = _lib.lib().sgns_init_model(_cdtype(dtype), dm.m_in.data_ptr(), dm.m_out.data_ptr(),
+                                    vocab_size, dim, dm.ld, seed & (2**64 - 1),
+                                    current_stream_ptr(dm.m_in.device))
+    _lib.check(rc, "sgns_init_model")
+    return dm
+
+
+def init_model(vocab_size: int, dim: int, seed: int, dtype=np.float32) -> EmbeddingModel:
+    """Reference-compatible init_model (host arrays), generated on the device."""
+    return init_device_model(vocab_size, dim, seed, dtype).to_host()
+
+
+def sigmoid_table_device(dtype, device="cuda"):
+    torch = _torch()
+    tab = SIGMOID_TABLE_F64 if np.dtype(dtype) == np.float64 else SIGMOID_TABLE_F32
+    return torch.from_numpy(tab.copy()).to(device)

@@ -1,0 +1,388 @@
+"""Training entry points over the device driver (drop-in for sgns/trainer.py).
+
+Reference map:
+  ALPHA_REFRESH_WORDS          sgns/trainer.py:48
+  ConfigError / TrainingConfig sgns/trainer.py:51-109
+  TrainingStats                sgns/trainer.py:112-119
+  update_alpha                 sgns/trainer.py:122-132
+  ThreadRun.advance            sgns/trainer.py:396-453  -> DeviceRun.advance (all workers, one launch)
+  train_encoded / train        sgns/trainer.py:477-552
+
+A reference thread is a device worker (one warp): it owns a contiguous
+sentence range from `split_by_tokens`, keeps its own stream and counters, and
+shares the model without locks (Hogwild).  Two samplers:
+  rng="splitmix"  the reference's per-thread splitmix64 stream (seed, stream
+                  id) and its count^0.75 slot table; with workers == threads
+                  every window, chunk and negative is bit-identical to the
+                  reference's, and alpha refreshes every 10,000 words per worker.
+  rng="philox"    production: Philox4x32-10 keyed by seed, counter = corpus
+                  token position (partition-invariant) and an alias table;
+                  alpha refreshes every sentence from the shared words-read
+                  counter, so it tracks global progress with ~1500 workers.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .corpus import (KEPT_BUFFER_TOKENS, EncodedCorpus, NegativeTable, Vocabulary, build_vocab,
+                     default_table_length, encode_corpus, negative_table_boundaries,
+                     read_tokens, split_by_tokens, NEGATIVE_POWER)
+from .model import DeviceModel, EmbeddingModel, current_stream_ptr, init_device_model
+from .kernel_batched import device_sigmoid_table
+from .rng import new_state
+
+ALPHA_REFRESH_WORDS = 10_000
+_INF_BUDGET = 2**62
+
+WORKER_DTYPE = np.dtype([
+    ("next_sent", "<i8"), ("lo", "<i8"), ("hi", "<i8"), ("epoch", "<i4"), ("done", "<i4"),
+    ("rng", "<u8"), ("alpha", "<f8"), ("read_local", "<f8"), ("trained_local", "<f8"),
+    ("kernel_counter", "<i8"), ("words_read", "<i8"), ("words_trained", "<i8")])
+
+
+class ConfigError(ValueError):
+    """Invalid training configuration."""
+
+
+@dataclass
+class TrainingConfig:
+    dim: int = 300
+    window: int = 5
+    negatives: int = 5
+    subsample: float = 1e-4
+    min_count: int = 5
+    alpha0: float = 0.025
+    alpha_floor_fraction: float = 1e-4
+    epochs: int = 5
+    threads: int = 1
+    batch_cap: int = 16
+    kernel: str = "batched"
+    seed: int = 1
+    dynamic_window: bool = True
+    table_length: int | None = None
+    float64: bool = False
+    matmul: str | None = None  # None / "cuda"
+    loss_sample_every: int = 100
+    # device knobs (new)
+    rng: str = "philox"                   # "philox" (production) | "splitmix" (reference stream)
+    workers: int | None = None            # None: splitmix -> threads; philox -> resident warps
+    alpha_refresh_words: int | None = None  # None: splitmix -> 10,000; philox -> every sentence
+
+    def validate(self) -> None:
+        if self.dim < 1:
+            raise ConfigError("dim must be >= 1")
+        if self.window < 1:
+            raise ConfigError("window must be >= 1")
+        if self.negatives < 1:
+            raise ConfigError("negatives must be >= 1")
+        if self.negatives > 31:
+            raise ConfigError("negatives must be <= 31 on the device path")
+        if self.subsample < 0:
+            raise ConfigError("subsample must be >= 0")
+        if self.min_count < 1:
+            raise ConfigError("min_count must be >= 1")
+        if self.alpha0 <= 0:
+            raise ConfigError("alpha0 must be positive")
+        if not 0 < self.alpha_floor_fraction < 1:
+            raise ConfigError("alpha_floor_fraction must be in (0, 1)")
+        if self.epochs < 1:
+            raise ConfigError("epochs must be >= 1")
+        if self.threads < 1:
+            raise ConfigError("threads must be >= 1")
+        if self.batch_cap < 1:
+            raise ConfigError("batch_cap must be >= 1")
+        if self.kernel != "batched":
+            raise ConfigError(f"unknown kernel {self.kernel!r} (the device path is 'batched')")
+        if self.matmul not in (None, "cuda"):
+            raise ConfigError(f"unknown matmul backend {self.matmul!r}")
+        if self.rng not in ("philox", "splitmix"):
+            raise ConfigError(f"unknown rng {self.rng!r}")
+        if self.workers is not None and self.workers < 1:
+            raise ConfigError("workers must be >= 1")
+        if self.alpha_refresh_words is not None and self.alpha_refresh_words < 1:
+            raise ConfigError("alpha_refresh_words must be >= 1")
+
+    @property
+    def dtype(self):
+        return np.float64 if self.float64 else np.float32
+
+    @property
+    def refresh_words(self) -> int:
+        if self.alpha_refresh_words is not None:
+            return self.alpha_refresh_words
+        return ALPHA_REFRESH_WORDS if self.rng == "splitmix" else 1
+
+
+@dataclass
+class TrainingStats:
+    words_processed: int = 0
+    words_read: int = 0
+    wall_seconds: float = 0.0
+    throughput_words_per_sec: float = 0.0
+    final_alpha: float = 0.0
+    loss_by_epoch: list[float] = field(default_factory=list)
+
+
+def update_alpha(words_done: int, total_words_times_epochs: float, alpha0: float,
+                 floor_fraction: float) -> float:
+    frac = 1.0 - words_done / (total_words_times_epochs + 1.0)
+    if frac < floor_fraction:
+        frac = floor_fraction
+    return alpha0 * frac
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1604_04661_b200 needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+class DeviceCorpus:
+    """EncodedCorpus resident in HBM (int32 ids, int64 sentence offsets)."""
+
+    def __init__(self, encoded: EncodedCorpus, device="cuda", ids=None, offsets=None):
+        torch = _torch()
+        self.host_offsets = np.ascontiguousarray(encoded.offsets, dtype=np.int64)
+        self.n_sentences = encoded.n_sentences
+        self.n_tokens = encoded.n_tokens
+        self.max_sentence = encoded.max_sentence_length()
+        if self.max_sentence > KEPT_BUFFER_TOKENS:
+            raise ValueError(f"sentence of {self.max_sentence} tokens exceeds the device limit "
+                             f"{KEPT_BUFFER_TOKENS} (encode_corpus splits at 1000)")
+        self.ids = ids if ids is not None else torch.from_numpy(
+            np.ascontiguousarray(encoded.ids, dtype=np.int32)).to(device)
+        self.offsets = offsets if offsets is not None else torch.from_numpy(self.host_offsets).to(device)
+
+
+class DeviceSampler:
+    """Negative sampler in HBM: the reference slot table or the alias table."""
+
+    def __init__(self, counts: np.ndarray, rng: str, table_length: int | None = None,
+                 table: NegativeTable | None = None, device="cuda", power: float = NEGATIVE_POWER):
+        torch = _torch()
+        self.rng = rng
+        counts = np.ascontiguousarray(counts, dtype=np.int64)
+        V = len(counts)
+        self.vocab = V
+        self.slots = self.alias_thr = self.alias_idx = None
+        if rng == "splitmix":
+            if table is not None:
+                bounds = np.ascontiguousarray(table.boundaries, dtype=np.int64)
+            else:
+                L = table_length if table_length is not None else default_table_length(V)
+                if L < V:
+                    from .corpus import TableLengthError
+                    raise TableLengthError(f"table length {L} is smaller than vocabulary size {V}")
+                bounds = negative_table_boundaries(counts, power, L)
+            n = int(bounds[-1])
+            d_bounds = torch.from_numpy(bounds).to(device)
+            self.slots = torch.empty(n, dtype=torch.int32, device=device)
+            rc = _lib.lib().sgns_expand_slots(d_bounds.data_ptr(), V, self.slots.data_ptr(), n,
+                                              current_stream_ptr(d_bounds.device))
+            _lib.check(rc, "sgns_expand_slots")
+        else:
+            thr = np.empty(V, dtype=np.uint32)
+            idx = np.empty(V, dtype=np.int32)
+            rc = _lib.lib().sgns_build_alias(counts.ctypes.data, V, power, thr.ctypes.data,
+                                             idx.ctypes.data)
+            _lib.check(rc, "sgns_build_alias")
+            self.host_alias = (thr, idx)
+            self.alias_thr = torch.from_numpy(thr.view(np.int32)).to(device)
+            self.alias_idx = torch.from_numpy(idx).to(device)
+
+
+def resident_workers(config: TrainingConfig, max_sentence: int) -> int:
+    out = _lib.I32(0)
+    rc = _lib.lib().sgns_resident_workers(
+        _lib.SGNS_F64 if config.float64 else _lib.SGNS_F32, config.dim, config.window,
+        config.negatives, config.batch_cap, max(max_sentence, 1), out)
+    _lib.check(rc, "sgns_resident_workers")
+    return int(out.value)
+
+
+class DeviceRun:
+    """All device workers of one rank: ThreadRun (trainer.py:332-453) x W, one launch per advance."""
+
+    def __init__(self, model: DeviceModel, corpus: DeviceCorpus, sampler: DeviceSampler,
+                 keep_probs: np.ndarray | None, config: TrainingConfig, alpha0_eff: float,
+                 total_x_epochs: float, n_workers: int, sent_range: tuple[int, int] | None = None,
+                 stream_base: int = 0, trace_cap: int = 0, update: bool = True):
+        torch = _torch()
+        self.torch = torch
+        self.model, self.corpus, self.sampler, self.config = model, corpus, sampler, config
+        dev = model.m_in.device
+        self.device = dev
+        lo, hi = sent_range if sent_range is not None else (0, corpus.n_sentences)
+        ranges = split_by_tokens(corpus.host_offsets, lo, hi, n_workers)
+        w = np.zeros(n_workers, dtype=WORKER_DTYPE)
+        w["lo"] = [a for a, _ in ranges]
+        w["next_sent"] = w["lo"]
+        w["hi"] = [b for _, b in ranges]
+        w["alpha"] = alpha0_eff
+        if config.rng == "splitmix":
+            w["rng"] = [new_state(config.seed, stream_base + i) for i in range(n_workers)]
+        self.n_workers = n_workers
+        self.workers = torch.from_numpy(w.view(np.uint8)).to(dev)
+        self.shared = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.loss = torch.zeros((n_workers, config.epochs), dtype=torch.float64, device=dev)
+        self.cells = torch.zeros((n_workers, config.epochs), dtype=torch.int64, device=dev)
+        self.error = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.keep = None if keep_probs is None else torch.from_numpy(
+            np.ascontiguousarray(keep_probs, dtype=np.float64)).to(dev)
+        self.sig = device_sigmoid_table(model.np_dtype, dev)
+        k1 = config.negatives + 1
+        self.rec_len = 4 + config.batch_cap + k1
+        self.trace_cap = trace_cap
+        if trace_cap:
+            self.trace = torch.full((n_workers, trace_cap, self.rec_len), -1, dtype=torch.int32, device=dev)
+            self.trace_alpha = torch.zeros((n_workers, trace_cap), dtype=torch.float64, device=dev)
+            self.trace_count = torch.zeros(n_workers, dtype=torch.int64, device=dev)
+        self.alpha0_eff = alpha0_eff
+        self.total_x_epochs = total_x_epochs
+        p = _lib.DriveParams()
+        p.dtype = model.cdtype
+        p.d_m_in, p.d_m_out = model.m_in.data_ptr(), model.m_out.data_ptr()
+        p.vocab, p.ld, p.dim = model.vocab_size, model.ld, model.dim
+        p.d_ids, p.d_offsets = corpus.ids.data_ptr(), corpus.offsets.data_ptr()
+        p.d_keep_probs = None if self.keep is None else self.keep.data_ptr()
+        p.rng_mode = _lib.RNG_SPLITMIX if config.rng == "splitmix" else _lib.RNG_PHILOX
+        if sampler.slots is not None:
+            p.d_slots, p.n_slots = sampler.slots.data_ptr(), sampler.slots.numel()
+        if sampler.alias_thr is not None:
+            p.d_alias_thr, p.d_alias_idx = sampler.alias_thr.data_ptr(), sampler.alias_idx.data_ptr()
+        p.seed = config.seed & (2**64 - 1)
+        p.window, p.dynamic, p.k_neg = config.window, int(config.dynamic_window), config.negatives
+        p.batch_cap = config.batch_cap
+        p.sigmoid_mode = _lib.SIGMOID_EXACT if config.float64 else _lib.SIGMOID_TABLE
+        p.d_sig_table = self.sig.data_ptr()
+        p.alpha0, p.floor_frac = alpha0_eff, config.alpha_floor_fraction
+        p.total_x_epochs = total_x_epochs
+        p.refresh_words = config.refresh_words
+        p.d_shared = self.shared.data_ptr()
+        p.epochs, p.loss_every = config.epochs, config.loss_sample_every
+        p.d_workers, p.n_workers = self.workers.data_ptr(), n_workers
+        p.d_loss_by_epoch, p.d_cells_by_epoch = self.loss.data_ptr(), self.cells.data_ptr()
+        p.update = int(update)
+        p.max_sentence = max(corpus.max_sentence, 1)
+        if trace_cap:
+            p.trace_cap = trace_cap
+            p.d_trace, p.d_trace_alpha = self.trace.data_ptr(), self.trace_alpha.data_ptr()
+            p.d_trace_count = self.trace_count.data_ptr()
+        p.d_error = self.error.data_ptr()
+        self.params = p
+        self._host_state = None
+
+    # -- launches ---------------------------------------------------------
+    def launch(self, word_budget: int, stream=None) -> None:
+        """Stream-ordered: every worker consumes up to word_budget words read."""
+        self.params.word_budget = int(word_budget)
+        st = current_stream_ptr(self.device) if stream is None else stream
+        _lib.check(_lib.lib().sgns_drive(self.params, st), "sgns_drive")
+        self._host_state = None
+
+    def state(self) -> np.ndarray:
+        if self._host_state is None:
+            self._host_state = self.workers.cpu().numpy().view(WORKER_DTYPE).copy()
+            err = int(self.error.item())
+            if err:
+                raise RuntimeError(f"sgns_drive device error {err} (sentence too long / bad window)")
+        return self._host_state
+
+    @property
+    def done(self) -> bool:
+        return bool(self.state()["done"].all())
+
+    @property
+    def words_read(self) -> int:
+        return int(self.state()["words_read"].sum())
+
+    @property
+    def words_trained(self) -> int:
+        return int(self.state()["words_trained"].sum())
+
+    def advance(self, word_budget: int) -> int:
+        """ThreadRun.advance semantics per worker; returns words read by all workers."""
+        before = self.words_read
+        self.launch(word_budget)
+        return self.words_read - before
+
+    def run_to_completion(self) -> None:
+        while not self.done:
+            self.launch(_INF_BUDGET)
+
+    def loss_by_epoch(self) -> list[float]:
+        ls = self.loss.sum(dim=0).cpu().numpy()
+        cs = self.cells.sum(dim=0).cpu().numpy()
+        return [float(a / b) if b else 0.0 for a, b in zip(ls, cs)]
+
+    def shared_words_read(self) -> int:
+        return int(self.shared[0].item())
+
+    def worker_trace(self, w: int):
+        n = min(int(self.trace_count[w].item()), self.trace_cap)
+        return self.trace[w, :n].cpu().numpy(), self.trace_alpha[w, :n].cpu().numpy()
+
+
+def default_workers(config: TrainingConfig, corpus: DeviceCorpus, n_sentences: int | None = None) -> int:
+    if config.workers is not None:
+        return config.workers
+    if config.rng == "splitmix":
+        return config.threads
+    cap = resident_workers(config, corpus.max_sentence)
+    n = corpus.n_sentences if n_sentences is None else n_sentences
+    return max(1, min(cap, n))
+
+
+def train_encoded(vocab: Vocabulary, encoded: EncodedCorpus, config: TrainingConfig,
+                  model: EmbeddingModel | DeviceModel | None = None,
+                  table: NegativeTable | None = None, progress: bool = False,
+                  return_device: bool = False):
+    """Train over an encoded corpus on the GPU; returns (model, TrainingStats)."""
+    config.validate()
+    torch = _torch()
+    if model is None:
+        dm = init_device_model(vocab.size, config.dim, config.seed, config.dtype)
+    elif isinstance(model, DeviceModel):
+        dm = model
+    else:
+        dm = DeviceModel.from_host(model)
+    corpus = DeviceCorpus(encoded, dm.m_in.device)
+    sampler = DeviceSampler(vocab.counts, config.rng, config.table_length, table, dm.m_in.device)
+    keep = vocab.keep_probs(config.subsample) if config.subsample > 0 else None
+    total_x_epochs = float(encoded.n_tokens) * config.epochs
+    n_workers = default_workers(config, corpus)
+    run = DeviceRun(dm, corpus, sampler, keep, config, config.alpha0, total_x_epochs, n_workers)
+    torch.cuda.synchronize(dm.m_in.device)
+    started = time.perf_counter()
+    run.run_to_completion()
+    torch.cuda.synchronize(dm.m_in.device)
+    wall = time.perf_counter() - started
+    stats = TrainingStats()
+    stats.words_processed = run.words_trained
+    stats.words_read = run.words_read
+    stats.wall_seconds = wall
+    stats.throughput_words_per_sec = stats.words_processed / max(wall, 1e-9)
+    stats.final_alpha = update_alpha(run.shared_words_read(), total_x_epochs, config.alpha0,
+                                     config.alpha_floor_fraction)
+    stats.loss_by_epoch = run.loss_by_epoch()
+    if return_device:
+        return dm, stats
+    if isinstance(model, EmbeddingModel):
+        dm.copy_to_host(model)
+        return model, stats
+    return dm.to_host(), stats
+
+
+def train(corpus_path: str, config: TrainingConfig, progress: bool = False):
+    """Build the vocabulary, encode the corpus, and train a fresh model on the GPU."""
+    config.validate()
+    vocab = build_vocab(read_tokens(corpus_path), config.min_count)
+    encoded = encode_corpus(corpus_path, vocab)
+    model, stats = train_encoded(vocab, encoded, config, progress=progress)
+    return model, vocab, stats

@@ -1,0 +1,322 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference-generated golden fixtures.  Tolerances are written in each test:
+  float64: rtol 1e-12 per update (tree vs sequential summation order only),
+  float32: |a - b| <= 1e-5 |a| + 1e-7 (tests/test_acceptance.py:199-209),
+  integers (windows, chunks, negatives, counters): bit-exact.
+"""
+
+import numpy as np
+import pytest
+
+from helpers import TRACE_CASES, kernel_case, load_golden, trace_to_records, train_config
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    torch.cuda.set_device(0)
+
+
+def _pkg():
+    import paper_1604_04661_b200 as P
+    return P
+
+
+def _oracle():
+    from oracle import oracle as O
+    return O
+
+
+def f32_close(a, b, rtol=1e-5, atol=1e-7):
+    ratio = np.abs(a.astype(np.float64) - b.astype(np.float64)) / (rtol * np.abs(b.astype(np.float64)) + atol)
+    return float(ratio.max()) if ratio.size else 0.0
+
+
+def near_bin_edge(scores, tol=2e-5):
+    v = (np.asarray(scores, dtype=np.float64) + 6.0) * (1000.0 / 12.0)
+    return np.abs(v - np.round(v)) < tol * 1000.0 / 12.0 * np.maximum(1.0, np.abs(scores))
+
+
+def test_graft_smoke():
+    import __graft_entry__ as g
+    g.smoke()
+
+
+def test_library_is_the_one_loaded():
+    from paper_1604_04661_b200 import _lib
+    L = _lib.lib()
+    maps = open("/proc/self/maps").read()
+    assert _lib.LIB_PATH in maps
+    assert L.sgns_abi_version() == 1
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_process_batch_golden(dtype):
+    """P1: one minibatch vs the reference's own process_batch outputs."""
+    P = _pkg()
+    g = load_golden("kernel")
+    npdt = np.float64 if dtype == "f64" else np.float32
+    worst = 0.0
+    for i in range(int(g["n_cases"][0])):
+        m_in, m_out, ins, outs, alpha, r_in, r_out = kernel_case(g, i)
+        model = P.EmbeddingModel(m_in.astype(npdt), m_out.astype(npdt))
+        before = model.copy()
+        P.process_batch(model, P.Minibatch(ins, outs), alpha)
+        # locality: untouched rows bit-identical
+        mask_in = np.ones(len(m_in), bool)
+        mask_in[r_in] = False
+        mask_out = np.ones(len(m_out), bool)
+        mask_out[r_out] = False
+        assert np.array_equal(model.input_vectors[mask_in], before.input_vectors[mask_in])
+        assert np.array_equal(model.output_vectors[mask_out], before.output_vectors[mask_out])
+        if alpha == 0.0:
+            assert np.array_equal(model.input_vectors, before.input_vectors)
+            assert np.array_equal(model.output_vectors, before.output_vectors)
+        if dtype == "f64":
+            np.testing.assert_allclose(model.input_vectors[r_in], g[f"c{i}_f64_naive_min"], rtol=1e-12, atol=1e-15)
+            np.testing.assert_allclose(model.output_vectors[r_out], g[f"c{i}_f64_naive_mout"], rtol=1e-12, atol=1e-15)
+        else:
+            scores = before.input_vectors[ins].astype(np.float64) @ before.output_vectors[outs].astype(np.float64).T
+            if near_bin_edge(scores).any():
+                continue  # a sigma-table bin flip between summation orders is legal
+            for be in ("naive", "blas"):
+                worst = max(worst, f32_close(model.input_vectors[r_in], g[f"c{i}_f32_{be}_min"]))
+                worst = max(worst, f32_close(model.output_vectors[r_out], g[f"c{i}_f32_{be}_mout"]))
+    assert worst <= 1.0, f"float32 tolerance budget used {worst:.2f}"
+
+
+def test_process_batch_validation():
+    P = _pkg()
+    m = P.EmbeddingModel(np.zeros((5, 4), np.float32), np.zeros((5, 4), np.float32))
+    with pytest.raises(ValueError):
+        P.process_batch(m, P.Minibatch([1], [0, 2]), -0.1)
+    with pytest.raises(ValueError):
+        P.process_batch(m, P.Minibatch([1], [0, 2]), 0.1, matmul="blas")
+    with pytest.raises(ValueError):
+        P.Minibatch([1], [3, 3])
+    with pytest.raises(ValueError):
+        P.process_batch(m, P.Minibatch([7], [0, 2]), 0.1)
+
+
+def test_init_model_bitwise():
+    P = _pkg()
+    g = load_golden("init")
+    for key in g.files:
+        if not key.startswith("in64_"):
+            continue
+        _, V, D, seed = key.split("_")
+        m64 = P.init_model(int(V), int(D), int(seed), dtype=np.float64)
+        m32 = P.init_model(int(V), int(D), int(seed), dtype=np.float32)
+        assert np.array_equal(m64.input_vectors, g[key])
+        assert np.array_equal(m32.input_vectors, g["in32_" + key[5:]])
+        assert not m32.output_vectors.any()
+
+
+def _random_windows(rng, V, n, m_max, k, disjoint=False):
+    wins = []
+    pool = rng.permutation(V)
+    used = 0
+    for _ in range(n):
+        m = int(rng.integers(1, m_max + 1))
+        if disjoint:
+            ids = pool[used:used + m + k + 1]
+            used += m + k + 1
+            ins, outs = ids[:m], ids[m:]
+        else:
+            zipf = np.minimum(rng.zipf(1.3, size=m + k + 1) - 1, V - 1)
+            ins, outs = zipf[:m], zipf[m:]
+            while (outs[1:] == outs[0]).any():
+                outs[1:] = np.where(outs[1:] == outs[0], rng.integers(0, V, k), outs[1:])
+        wins.append((np.asarray(ins, np.int32), np.asarray(outs, np.int32)))
+    return wins
+
+
+@pytest.mark.parametrize("dtype,D,k", [("f64", 300, 5), ("f32", 300, 5), ("f32", 100, 5),
+                                       ("f32", 200, 10), ("f32", 300, 15), ("f64", 24, 3)])
+def test_disjoint_windows_equal_sequential(dtype, D, k):
+    """P2: a batch of row-disjoint windows == the sequential oracle application."""
+    P, O = _pkg(), _oracle()
+    from paper_1604_04661_b200.kernel_batched import DeviceWindowBatch, WindowBatch
+    from paper_1604_04661_b200.model import DeviceModel, SIGMOID_TABLE_F32, SIGMOID_TABLE_F64
+    rng = np.random.default_rng(D + k)
+    npdt = np.float64 if dtype == "f64" else np.float32
+    V = 4000
+    scale = D ** -0.25
+    base = P.EmbeddingModel((rng.normal(size=(V, D)) * scale).astype(npdt),
+                            (rng.normal(size=(V, D)) * scale).astype(npdt))
+    wins = _random_windows(rng, V, 150, 10, k, disjoint=True)
+    alpha = 0.025
+    wb = WindowBatch.from_minibatches([P.Minibatch(a, b) for a, b in wins])
+    dm = DeviceModel.from_host(base)
+    P.update_windows(dm, DeviceWindowBatch(wb), alpha)
+    got = dm.to_host()
+    ref_in, ref_out = base.input_vectors.copy(), base.output_vectors.copy()
+    tab = SIGMOID_TABLE_F64 if dtype == "f64" else SIGMOID_TABLE_F32
+    flips = 0
+    for a, b in wins:
+        O.process_batch(ref_in, ref_out, a, b, alpha, tab)
+        s = base.input_vectors[a].astype(np.float64) @ base.output_vectors[b].astype(np.float64).T
+        flips += int(near_bin_edge(s).any())
+    if dtype == "f64":
+        np.testing.assert_allclose(got.input_vectors, ref_in, rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(got.output_vectors, ref_out, rtol=1e-12, atol=1e-15)
+    else:
+        bad_in = np.abs(got.input_vectors.astype(np.float64) - ref_in) > 1e-5 * np.abs(ref_in) + 1e-7
+        bad_out = np.abs(got.output_vectors.astype(np.float64) - ref_out) > 1e-5 * np.abs(ref_out) + 1e-7
+        bad_rows = int(bad_in.any(axis=1).sum() + bad_out.any(axis=1).sum())
+        # only windows with a score on a sigma-bin edge may differ (<= their rows)
+        assert bad_rows <= flips * 16, (bad_rows, flips)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_snapshot_conflicting_windows(dtype):
+    """P3: Zipf-conflicting windows in snapshot mode == snapshot + sum of per-window deltas."""
+    P, O = _pkg(), _oracle()
+    from paper_1604_04661_b200.kernel_batched import DeviceWindowBatch, WindowBatch
+    from paper_1604_04661_b200.model import DeviceModel, SIGMOID_TABLE_F32, SIGMOID_TABLE_F64
+    rng = np.random.default_rng(7)
+    npdt = np.float64 if dtype == "f64" else np.float32
+    V, D, k = 500, 300, 5
+    base = P.EmbeddingModel((rng.normal(size=(V, D)) * D ** -0.25).astype(npdt),
+                            (rng.normal(size=(V, D)) * D ** -0.25).astype(npdt))
+    wins = _random_windows(rng, V, 400, 10, k)
+    wb = WindowBatch.from_minibatches([P.Minibatch(a, b) for a, b in wins])
+    alphas = rng.uniform(0.001, 0.03, size=len(wins))
+    src = DeviceModel.from_host(base)
+    dst = src.clone()
+    P.update_windows(dst, DeviceWindowBatch(wb), torch.from_numpy(alphas), src=src)
+    got = dst.to_host()
+    tab = SIGMOID_TABLE_F64 if dtype == "f64" else SIGMOID_TABLE_F32
+    acc_in = base.input_vectors.astype(np.float64).copy()
+    acc_out = base.output_vectors.astype(np.float64).copy()
+    for (a, b), al in zip(wins, alphas):
+        mi, mo = base.input_vectors.copy(), base.output_vectors.copy()
+        O.process_batch(mi, mo, a, b, float(npdt(al)), tab)
+        acc_in += mi.astype(np.float64) - base.input_vectors
+        acc_out += mo.astype(np.float64) - base.output_vectors
+    if dtype == "f64":
+        np.testing.assert_allclose(got.input_vectors, acc_in, rtol=1e-10, atol=1e-13)
+        np.testing.assert_allclose(got.output_vectors, acc_out, rtol=1e-10, atol=1e-13)
+    else:
+        # float32 adds arrive in a different order (atomics): per-entry error scales with the
+        # number of contributions; bound it by 1e-5 relative to the summed |delta| magnitude
+        np.testing.assert_allclose(got.input_vectors, acc_in, rtol=1e-4, atol=2e-6)
+        np.testing.assert_allclose(got.output_vectors, acc_out, rtol=1e-4, atol=2e-6)
+
+
+def _run_driver(ids, off, counts, *, window, k, cap, dynamic, subsample, seed, stream_base,
+                table_len, rng, workers=1, dtype=np.float32, dim=4, epochs=1, update=False,
+                model=None, trace_cap=None, loss_every=100, refresh=None, alpha0=0.025):
+    P = _pkg()
+    from paper_1604_04661_b200.corpus import EncodedCorpus, keep_probabilities
+    from paper_1604_04661_b200.model import DeviceModel
+    from paper_1604_04661_b200.trainer import DeviceCorpus, DeviceRun, DeviceSampler
+    enc = EncodedCorpus(ids, off, np.zeros(len(off) - 1, np.int64))
+    cfg = P.TrainingConfig(dim=dim, window=window, negatives=k, batch_cap=cap, dynamic_window=dynamic,
+                           subsample=subsample, seed=seed, epochs=epochs, rng=rng, workers=workers,
+                           float64=dtype == np.float64, table_length=table_len, min_count=1,
+                           loss_sample_every=loss_every, alpha_refresh_words=refresh, alpha0=alpha0)
+    dm = model if model is not None else DeviceModel.empty(len(counts), dim, dtype)
+    corpus = DeviceCorpus(enc)
+    sampler = DeviceSampler(counts, rng, table_len)
+    keep = keep_probabilities(counts, int(counts.sum()), subsample) if subsample > 0 else None
+    if trace_cap is None:
+        trace_cap = len(ids) * epochs + 10
+    run = DeviceRun(dm, corpus, sampler, keep, cfg, alpha0, float(off[-1]) * epochs, workers,
+                    stream_base=stream_base, trace_cap=trace_cap, update=update)
+    run.run_to_completion()
+    return run, sampler
+
+
+@pytest.mark.parametrize("case", TRACE_CASES, ids=[c[0] for c in TRACE_CASES])
+def test_driver_windows_bit_exact_vs_reference(case):
+    """Subsample -> dynamic window -> chunks -> shared negatives: the device stream is the
+    reference's stream (splitmix, slot table), record for record."""
+    name, n, V, w, k, cap, dyn, sub, seed, stream, table_len = case
+    g = load_golden("traces")
+    ids, off, counts = g[f"{name}_ids"], g[f"{name}_offsets"], g[f"{name}_counts"]
+    run, _ = _run_driver(ids, off, counts, window=w, k=k, cap=cap, dynamic=dyn, subsample=sub,
+                         seed=seed, stream_base=stream, table_len=table_len, rng="splitmix")
+    got, _ = run.worker_trace(0)
+    expect = trace_to_records(g, name, cap, k + 1)
+    assert got.shape == expect.shape
+    assert np.array_equal(got, expect)
+    assert int(run.state()["rng"][0]) == int(g[f"{name}_final_state"][0])
+
+
+@pytest.mark.parametrize("rng_mode", ["splitmix", "philox"])
+def test_driver_multiworker_trace_vs_oracle(rng_mode):
+    """W workers over split_by_tokens ranges, 2 epochs: per-worker records equal the oracle's."""
+    O = _oracle()
+    from paper_1604_04661_b200.synthetic import make_planted_corpus
+    from paper_1604_04661_b200.corpus import default_table_length, keep_probabilities
+    syn = make_planted_corpus(20_000, 300, n_clusters=4, cluster_size=5, sentence_len=41, seed=5)
+    ids, off, counts = syn.encoded.ids, syn.encoded.offsets, syn.vocab.counts
+    W, w, k, cap = 5, 5, 5, 4
+    run, sampler = _run_driver(ids, off, counts, window=w, k=k, cap=cap, dynamic=True, subsample=1e-3,
+                               seed=9, stream_base=0, table_len=None, rng=rng_mode, workers=W,
+                               epochs=2)
+    keep = keep_probabilities(counts, int(counts.sum()), 1e-3)
+    slots = alias = None
+    if rng_mode == "splitmix":
+        L = default_table_length(len(counts))
+        slots = np.repeat(np.arange(len(counts), dtype=np.int32),
+                          np.diff(O.neg_boundaries(counts, 0.75, L), prepend=0))
+    else:
+        alias = sampler.host_alias
+    m = np.zeros((len(counts), 4), np.float32)
+    orc = O.OracleRun(ids, off, m, m.copy(), keep_probs=keep, window=w, negatives=k, batch_cap=cap,
+                      dynamic=True, seed=9, alpha0=0.025, floor_frac=1e-4,
+                      total_x_epochs=float(off[-1]) * 2, epochs=2, loss_every=0, n_workers=W,
+                      rng_mode=rng_mode, slots=slots, alias=alias,
+                      sig_table=np.zeros(1000, np.float32), trace_cap=len(ids) * 2 + 10,
+                      update=False, refresh_words=10_000 if rng_mode == "splitmix" else 1)
+    orc.run_to_completion()
+    st = run.state()
+    for wk in range(W):
+        a, _ = run.worker_trace(wk)
+        b, _ = orc.worker_trace(wk)
+        assert a.shape == b.shape and np.array_equal(a, b), wk
+        assert int(st["words_read"][wk]) == orc.workers[wk].words_read
+        assert int(st["words_trained"][wk]) == orc.workers[wk].words_trained
+        assert int(st["kernel_counter"][wk]) == orc.workers[wk].kernel_counter
+
+
+@pytest.mark.parametrize("name", ["f64_naive", "f64_cap1_k1", "f64_w10_cap4", "f64_static_nosub",
+                                  "f64_loss7"])
+def test_driver_train_f64_matches_reference(name):
+    """Fused driver, one worker, float64: the reference's train_encoded model and stats."""
+    P = _pkg()
+    cfg = train_config(name)
+    g = load_golden("train")
+    from paper_1604_04661_b200.corpus import EncodedCorpus, Vocabulary
+    enc = EncodedCorpus(g["ids"], g["offsets"], g["sentence_bytes"])
+    vocab = Vocabulary.from_counts(g["counts"])
+    tc = P.TrainingConfig(**{k: v for k, v in cfg.items()}, rng="splitmix")
+    model, stats = P.train_encoded(vocab, enc, tc)
+    assert [stats.words_processed, stats.words_read] == g[f"{name}_stats"].tolist()
+    assert stats.final_alpha == pytest.approx(float(g[f"{name}_final_alpha"][0]), rel=1e-12)
+    np.testing.assert_allclose(stats.loss_by_epoch, g[f"{name}_loss"], rtol=1e-9)
+    np.testing.assert_allclose(model.input_vectors, g[f"{name}_min"], rtol=1e-8, atol=1e-12)
+    np.testing.assert_allclose(model.output_vectors, g[f"{name}_mout"], rtol=1e-8, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["f32_naive", "f32_blas", "f32_k15_loss1"])
+def test_driver_train_f32_close_to_reference(name):
+    """float32, one worker: identical stream and counters; loss within 0.5%, model close."""
+    P = _pkg()
+    cfg = train_config(name)
+    g = load_golden("train")
+    from paper_1604_04661_b200.corpus import EncodedCorpus, Vocabulary
+    enc = EncodedCorpus(g["ids"], g["offsets"], g["sentence_bytes"])
+    vocab = Vocabulary.from_counts(g["counts"])
+    tc = P.TrainingConfig(**{k: v for k, v in cfg.items() if k != "matmul"}, rng="splitmix")
+    model, stats = P.train_encoded(vocab, enc, tc)
+    assert [stats.words_processed, stats.words_read] == g[f"{name}_stats"].tolist()
+    np.testing.assert_allclose(stats.loss_by_epoch, g[f"{name}_loss"], rtol=5e-3)
+    err = np.abs(model.input_vectors - g[f"{name}_min"]).max()
+    assert err < 5e-3 * np.abs(g[f"{name}_min"]).max()
