@@ -225,7 +225,7 @@ def _run_driver(ids, off, counts, *, window, k, cap, dynamic, subsample, seed, s
     sampler = DeviceSampler(counts, rng, table_len)
     keep = keep_probabilities(counts, int(counts.sum()), subsample) if subsample > 0 else None
     if trace_cap is None:
-        trace_cap = len(ids) * epochs + 10
+        trace_cap = len(ids) * epochs * (-(-2 * window // cap)) + 10
     run = DeviceRun(dm, corpus, sampler, keep, cfg, alpha0, float(off[-1]) * epochs, workers,
                     stream_base=stream_base, trace_cap=trace_cap, update=update)
     run.run_to_completion()
@@ -273,7 +273,7 @@ def test_driver_multiworker_trace_vs_oracle(rng_mode):
                       dynamic=True, seed=9, alpha0=0.025, floor_frac=1e-4,
                       total_x_epochs=float(off[-1]) * 2, epochs=2, loss_every=0, n_workers=W,
                       rng_mode=rng_mode, slots=slots, alias=alias,
-                      sig_table=np.zeros(1000, np.float32), trace_cap=len(ids) * 2 + 10,
+                      sig_table=np.zeros(1000, np.float32), trace_cap=len(ids) * 2 * 3 + 10,
                       update=False, refresh_words=10_000 if rng_mode == "splitmix" else 1)
     orc.run_to_completion()
     st = run.state()
