@@ -1,0 +1,424 @@
+"""Benchmark of the pSGNScc hot path on B200 (BASELINE.json configs[3] by default).
+
+Metric: trained (kept, post-subsample) words per second, whole job (all GPUs),
+d=300, w=5, K=5, t=1e-4, on a seeded synthetic 800M-token Zipf(1.05) corpus
+over 1M ids (min-count 5) with planted clusters (data: synthetic).  A step is
+one sync period: every GPU's workers read 1M words of their shard through the
+fused device driver, then (N > 1) the full model is averaged with NCCL.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--impl reference` times the CPU restatement of the reference algorithm
+(oracle/, kind "port": splitmix stream, 10^8-slot negative table, float64
+accumulation, one pthread per host core, Hogwild) on the same corpus, config,
+metric and step definition, on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training words/sec at 1/2/4/8 B200 and achieved HBM GB/s vs peak (d=300,w=5,K=5)"
+UNIT = "words/s"
+DIM, WINDOW, NEG, SUBSAMPLE, ALPHA0 = 300, 5, 5, 1e-4, 0.025
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--tokens", type=int, default=800_000_000)
+    ap.add_argument("--vocab", type=int, default=1_000_000)
+    ap.add_argument("--period", type=int, default=1_000_000, help="words read per GPU per step")
+    ap.add_argument("--workers", type=int, default=0, help="device workers (0: resident warps)")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        self.index = index
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 6:
+                    continue
+                try:
+                    sm.append(float(f[0]))
+                    smax.append(float(f[1]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, f[2:6]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def build_corpus(args, device):
+    from paper_1604_04661_b200.synthetic import make_planted_corpus_device
+    return make_planted_corpus_device(args.tokens, args.vocab, zipf_s=1.05, min_count=5,
+                                      seed=args.seed, device=device)
+
+
+def shard_of(corpus, world, rank):
+    from paper_1604_04661_b200.corpus import EncodedCorpus, partition_sentences
+    enc = EncodedCorpus(np.empty(0, np.int32), corpus.host_offsets(), corpus.sentence_bytes)
+    return enc, partition_sentences(enc, world)[rank]
+
+
+# ------------------------------------------------------------------ CPU leg ----
+def cpu_reference_run(corpus, enc, shard, args, seconds=None, steps=None, warmup=0):
+    """The oracle (reference restatement) on host cores: splitmix + slot table, T pthreads."""
+    from oracle import oracle as O
+    from paper_1604_04661_b200.corpus import default_table_length, keep_probabilities
+    T = len(os.sched_getaffinity(0))
+    counts = corpus.counts
+    V = len(counts)
+    need_tokens = args.period * ((steps or 0) + warmup + 2) if steps else args.period * 64
+    off = enc.offsets
+    lo = shard[0]
+    hi = int(np.searchsorted(off, off[lo] + need_tokens)) if need_tokens < off[shard[1]] - off[lo] else shard[1]
+    hi = max(hi, lo + 1)
+    ids = corpus.ids[off[lo]:off[hi]].cpu().numpy()
+    sub_off = (off[lo:hi + 1] - off[lo]).astype(np.int64)
+    keep = keep_probabilities(counts, int(counts.sum()), SUBSAMPLE)
+    L = default_table_length(V)
+    slots = np.repeat(np.arange(V, dtype=np.int32), np.diff(O.neg_boundaries(counts, 0.75, L), prepend=0))
+    from paper_1604_04661_b200.model import SIGMOID_TABLE_F32
+    m_in = O.init_model(V, DIM, args.seed).astype(np.float32)
+    m_out = np.zeros((V, DIM), np.float32)
+    total = float(enc.n_tokens)
+    run = O.OracleRun(ids, sub_off, m_in, m_out, keep_probs=keep, window=WINDOW, negatives=NEG,
+                      batch_cap=16, dynamic=True, seed=args.seed, alpha0=ALPHA0, floor_frac=1e-4,
+                      total_x_epochs=total, epochs=1, loss_every=100, n_workers=T, slots=slots,
+                      sig_table=SIGMOID_TABLE_F32, refresh_words=10_000)
+    budget = math.ceil(args.period / T)
+    for _ in range(warmup):
+        run.advance(budget, T)
+    t0_tr = sum(w.words_trained for w in run.workers)
+    t0_rd = sum(w.words_read for w in run.workers)
+    n = 0
+    start = time.perf_counter()
+    while True:
+        run.advance(budget, T)
+        n += 1
+        el = time.perf_counter() - start
+        if steps is not None and n >= steps:
+            break
+        if steps is None and (el >= seconds and n >= 3):
+            break
+        if run.done:
+            break
+    el = time.perf_counter() - start
+    trained = sum(w.words_trained for w in run.workers) - t0_tr
+    read = sum(w.words_read for w in run.workers) - t0_rd
+    return {"value": trained / el, "unit": UNIT, "cores": T, "kind": "port",
+            "sample": f"{n} steps x {args.period} words read (= {read} read, {trained} trained) of the "
+                      f"same corpus, splitmix + 1e8-slot table, {T} pthreads, float32 model V={V} d={DIM}",
+            "seconds": el, "steps": n}
+
+
+def run_reference_arm(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    import torch
+    dev = f"cuda:{local}" if torch.cuda.is_available() else "cpu"
+    corpus = build_corpus(args, dev)  # data generation only (torch); no package kernels
+    enc, shard = shard_of(corpus, 1, 0)
+    res = cpu_reference_run(corpus, enc, shard, args, steps=args.steps, warmup=args.warmup)
+    line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * res["seconds"] / max(res["steps"], 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": config_block(args, world),
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, world):
+    return {"workload": "configs[3] large corpus: 800M-token seeded Zipf(1.05) over 1M ids, planted "
+                        "clusters, min-count 5, d=300 w=5 K=5 t=1e-4, 1 epoch; step = 1M words read "
+                        "per GPU (+ full-model NCCL average when N>1)",
+            "tokens": args.tokens, "vocab_raw": args.vocab, "dim": DIM, "window": WINDOW,
+            "negatives": NEG, "subsample": SUBSAMPLE, "period_words_per_gpu": args.period,
+            "parallelism": f"dp{world}",
+            "l2": "model 2.4 GB and corpus 3.2 GB exceed the 126 MB L2; no flush between steps"}
+
+
+# --------------------------------------------------------------- GPU leg ----
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1604_04661_b200 import _lib
+    from paper_1604_04661_b200.distributed import NcclTransport, scaled_alpha0
+    from paper_1604_04661_b200.model import init_device_model
+    from paper_1604_04661_b200.trainer import (DeviceCorpus, DeviceRun, DeviceSampler, StreamingTrainer,
+                                               TrainingConfig, resident_workers)
+    from paper_1604_04661_b200.corpus import keep_probabilities
+
+    t_gen = time.perf_counter()
+    corpus = build_corpus(args, dev)
+    enc, shard = shard_of(corpus, world, rank)
+    t_gen = time.perf_counter() - t_gen
+    counts = corpus.counts
+    V = len(counts)
+    # configs[3] is one epoch; if --steps asks for more words than the shard holds, the
+    # workers wrap into further epochs so every timed step does a full period of work
+    shard_tokens = int(enc.offsets[shard[1]] - enc.offsets[shard[0]])
+    epochs = max(1, math.ceil((args.warmup + args.steps + 1) * args.period / max(shard_tokens, 1)))
+    cfg = TrainingConfig(dim=DIM, window=WINDOW, negatives=NEG, subsample=SUBSAMPLE, min_count=5,
+                         alpha0=ALPHA0, epochs=epochs, seed=args.seed, rng="philox")
+    dcorp = DeviceCorpus(enc, dev, ids=corpus.ids, offsets=corpus.offsets)
+    model = init_device_model(V, DIM, args.seed, np.float32, dev)
+    sampler = DeviceSampler(counts, "philox", device=dev)
+    keep = keep_probabilities(counts, int(counts.sum()), SUBSAMPLE)
+    W = args.workers or resident_workers(cfg, corpus.max_sentence)
+    alpha0_eff = scaled_alpha0(ALPHA0, world)
+    total_x = float(corpus.n_tokens) * epochs / world
+    run = DeviceRun(model, dcorp, sampler, keep, cfg, alpha0_eff, total_x, W, sent_range=shard,
+                    stream_base=rank * W)
+    transport = NcclTransport() if world > 1 else None
+    budget = math.ceil(args.period / W)
+    stream = torch.cuda.current_stream(dev)
+    all_rows = np.arange(V, dtype=np.int64)
+    wv = run.workers.view(torch.int64).view(W, 12)
+
+    def counters():
+        return torch.stack([wv[:, 10].sum(), wv[:, 9].sum(), wv[:, 11].sum(), wv[:, 8].sum()])
+
+    k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)]
+
+    def step(i=None):
+        if i is not None:
+            k_ev[i][0].record(stream)
+        run.launch(budget)
+        if i is not None:
+            k_ev[i][1].record(stream)
+        if transport is not None:
+            transport.allreduce_average(model.m_in, all_rows, "in")
+            transport.allreduce_average(model.m_out, all_rows, "out")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    c0 = counters()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t_start.record(stream)
+    for i in range(args.steps):
+        step(i)
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    kernel_ms = [a.elapsed_time(b) for a, b in k_ev]
+    c1 = counters()
+    d = (c1 - c0).double()
+    if run.done:
+        print("warning: shard exhausted during timing; use more tokens", file=sys.stderr)
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    tot = d.clone()
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    max_ms = float(t.item())
+    trained, read, inputs, chunks = [float(x) for x in tot.cpu().tolist()]
+    value = trained / (max_ms / 1000.0)
+    # roofline of the fused driver kernel (this rank): algorithmic bytes of every chunk
+    my = [float(x) for x in d.cpu().tolist()]
+    k1 = NEG + 1
+    bytes_step = 2.0 * 4.0 * DIM * (my[2] + k1 * my[3]) / args.steps
+    flops_step = 6.0 * DIM * k1 * my[2] / args.steps
+    avg_kernel_s = float(np.mean(kernel_ms)) / 1000.0
+    peak, peak_kind = measured_peaks()
+    achieved = bytes_step / avg_kernel_s / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                "kernel": "drive_kernel<float,3,CREG,6,PHILOX>",
+                "algorithmic_bytes_per_launch": bytes_step,
+                "gflops": flops_step / avg_kernel_s / 1e9,
+                "avg_launch_ms": avg_kernel_s * 1000.0,
+                "mean_inputs_per_chunk": my[2] / max(my[3], 1.0)}
+    traffic_path = os.path.join(ROOT, "profiles", "drive_kernel_traffic.json")
+    if os.path.exists(traffic_path):
+        with open(traffic_path) as fh:
+            roofline["traffic"] = json.load(fh).get("dram_bytes_per_launch")
+
+    # ---- e2e: the public streaming API from pinned host buffers (H2D + D2H in the timed region)
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_leg(args, corpus, enc, shard, cfg, counts, keep, world, rank, dev, alpha0_eff, total_x)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        del run, model, sampler
+        torch.cuda.empty_cache()
+        cpu = cpu_reference_run(corpus, enc, shard, args, seconds=args.cpu_seconds, warmup=1)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": config_block(args, world), "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": args.steps, "clocks": clk,
+                "words_read_per_sec": read / (max_ms / 1000.0),
+                "workers_per_gpu": W, "corpus_gen_seconds": t_gen}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_leg(args, corpus, enc, shard, cfg, counts, keep, world, rank, dev, alpha0_eff, total_x):
+    """Same metric through the public streaming API: each step copies its ~1M-token
+    sentence chunk from pinned host memory, trains it, and reads back its counters."""
+    import torch
+    import torch.distributed as dist
+    from paper_1604_04661_b200.model import init_device_model
+    from paper_1604_04661_b200.trainer import StreamingTrainer
+
+    off = enc.offsets
+    lo_s, hi_s = shard
+    n_chunks = args.warmup + args.steps
+    # chunk boundaries: consecutive sentence ranges of ~period tokens from the shard start
+    bounds = [lo_s]
+    for _ in range(n_chunks):
+        target = off[bounds[-1]] + args.period
+        nxt = int(np.searchsorted(off, target, side="left"))
+        nxt = min(max(nxt, bounds[-1] + 1), hi_s)
+        bounds.append(nxt)
+    tok_lo, tok_hi = int(off[bounds[0]]), int(off[bounds[-1]])
+    host_ids = torch.empty(tok_hi - tok_lo, dtype=torch.int32).pin_memory()
+    host_ids.copy_(corpus.ids[tok_lo:tok_hi].cpu())
+    max_tok = max(int(off[b] - off[a]) for a, b in zip(bounds[:-1], bounds[1:]))
+    max_sent = max(b - a for a, b in zip(bounds[:-1], bounds[1:]))
+    model = init_device_model(len(counts), DIM, args.seed + 17, np.float32, dev)
+    st = StreamingTrainer(model, counts, cfg, total_x, max_tok, max_sent, corpus.max_sentence,
+                          alpha0_eff=alpha0_eff, keep_probs=keep)
+    stream = torch.cuda.current_stream(dev)
+
+    def chunk(i):
+        a, b = bounds[i], bounds[i + 1]
+        base = int(off[a])
+        return st.train_chunk(host_ids[base - tok_lo:int(off[b]) - tok_lo], off[a:b + 1] - base, base)
+
+    for i in range(args.warmup):
+        chunk(i)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    wall0 = time.perf_counter()
+    trained = 0
+    h2d = d2h = 0
+    for i in range(args.warmup, n_chunks):
+        tr, rd, ls, cl, inp, ch = chunk(i)
+        trained += tr
+        h2d += st.h2d_bytes
+        d2h += st.d2h_bytes
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - wall0
+    ms = t0.elapsed_time(t1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    tr_t = torch.tensor([float(trained)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tr_t, op=dist.ReduceOp.SUM)
+    value = float(tr_t.item()) / (float(t.item()) / 1000.0)
+    del st, model
+    torch.cuda.empty_cache()
+    return {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
+            "d2h_bytes_per_step": d2h // args.steps, "wall_seconds": wall,
+            "api": "StreamingTrainer.train_chunk (pinned host chunk -> sgns_drive -> counters)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -54,6 +54,7 @@ typedef struct sgns_worker {
   uint64_t rng;                       /* splitmix64 state (SGNS_RNG_SPLITMIX) */
   double alpha, read_local, trained_local;
   int64_t kernel_counter, words_read, words_trained;
+  int64_t inputs;                     /* sum of chunk input counts (roofline accounting) */
 } sgns_worker;
 
 /* One batch of packed windows (the CSR form of a list of Minibatch,
@@ -106,6 +107,8 @@ typedef struct sgns_drive_params {
   int64_t *d_trace_count;        /* [n_workers] */
   int32_t *d_error;              /* may be NULL */
   int32_t warps_per_block;       /* 0: default */
+  int64_t token_base;            /* PHILOX: corpus position of d_ids[0] (streamed chunks) */
+  int32_t epoch_base;            /* PHILOX: epoch index added to each worker's epoch */
 } sgns_drive_params;
 
 /* Fused resumable driver: every worker consumes up to word_budget words read. */
@@ -130,6 +133,8 @@ int sgns_resident_workers(int32_t dtype, int32_t dim, int32_t window, int32_t k_
 
 const char *sgns_error_string(int32_t code);
 int sgns_abi_version(void);
+/* sizeof(sgns_worker), sizeof(sgns_drive_params): lets bindings check their layout. */
+int sgns_struct_sizes(int32_t *worker_bytes, int32_t *params_bytes);
 
 #ifdef __cplusplus
 }

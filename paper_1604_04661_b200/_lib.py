@@ -24,7 +24,8 @@ I32, I64, U64, F64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
 class SgnsWorker(C.Structure):
     _fields_ = [("next_sent", I64), ("lo", I64), ("hi", I64), ("epoch", I32), ("done", I32),
                 ("rng", U64), ("alpha", F64), ("read_local", F64), ("trained_local", F64),
-                ("kernel_counter", I64), ("words_read", I64), ("words_trained", I64)]
+                ("kernel_counter", I64), ("words_read", I64), ("words_trained", I64),
+                ("inputs", I64)]
 
 
 class DriveParams(C.Structure):
@@ -39,7 +40,7 @@ class DriveParams(C.Structure):
         ("n_workers", I32), ("word_budget", I64), ("d_loss_by_epoch", P),
         ("d_cells_by_epoch", P), ("update", I32), ("max_sentence", I32), ("trace_cap", I64),
         ("d_trace", P), ("d_trace_alpha", P), ("d_trace_count", P), ("d_error", P),
-        ("warps_per_block", I32),
+        ("warps_per_block", I32), ("token_base", I64), ("epoch_base", I32),
     ]
 
 
@@ -76,14 +77,22 @@ def lib() -> C.CDLL:
     L.sgns_build_alias.argtypes = [P, I64, F64, P, P]
     L.sgns_resident_workers.restype = C.c_int
     L.sgns_resident_workers.argtypes = [I32, I32, I32, I32, I32, I32, C.POINTER(I32)]
+    L.sgns_struct_sizes.restype = C.c_int
+    L.sgns_struct_sizes.argtypes = [C.POINTER(I32), C.POINTER(I32)]
     if L.sgns_abi_version() != 1:
         raise LibraryMissing("libsgns_b200.so ABI version mismatch; rebuild")
+    wb, pb = I32(0), I32(0)
+    L.sgns_struct_sizes(C.byref(wb), C.byref(pb))
+    if (wb.value, pb.value) != (C.sizeof(SgnsWorker), C.sizeof(DriveParams)):
+        raise LibraryMissing(f"struct layout mismatch: C ({wb.value}, {pb.value}) vs ctypes "
+                             f"({C.sizeof(SgnsWorker)}, {C.sizeof(DriveParams)}); rebuild")
     _lib = L
     return L
 
 
 EXPORTED = ("sgns_update_windows", "sgns_drive", "sgns_init_model", "sgns_expand_slots",
-            "sgns_build_alias", "sgns_resident_workers", "sgns_error_string", "sgns_abi_version")
+            "sgns_build_alias", "sgns_resident_workers", "sgns_error_string", "sgns_abi_version",
+            "sgns_struct_sizes")
 
 
 class SgnsError(RuntimeError):

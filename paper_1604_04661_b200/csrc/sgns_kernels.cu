@@ -139,6 +139,8 @@ template <typename T> struct DriveArgs {
   int64_t *trace_count;
   int32_t *error;
   int wpb;
+  int64_t token_base;
+  uint32_t epoch_base;
 };
 
 // Splitmix stream window: 32 consecutive draws evaluated by the 32 lanes.
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(256) drive_kernel(DriveArgs<T> p) {
   double alpha = S.alpha, read_local = S.read_local, trained_local = S.trained_local;
   T alpha_t = (T)alpha;
   uint64_t rng = S.rng;
-  int64_t s = S.next_sent, budget_used = 0, trained = 0, kc = S.kernel_counter;
+  int64_t s = S.next_sent, budget_used = 0, trained = 0, kc = S.kernel_counter, inputs = 0;
   int epoch = S.epoch;
   int done = 0;
   double loss = 0.0;
@@ -242,7 +244,8 @@ __global__ void __launch_bounds__(256) drive_kernel(DriveArgs<T> p) {
         if (RNG == SGNS_RNG_SPLITMIX) {
           u = u53(sm_mix(rng + (uint64_t)(i + 1) * kGolden));
         } else {
-          const uint4 o = philox_tok((uint64_t)(lo_t + i), (uint32_t)epoch, kTagSub, p.key0, p.key1);
+          const uint4 o = philox_tok((uint64_t)(p.token_base + lo_t + i), p.epoch_base + (uint32_t)epoch,
+                                     kTagSub, p.key0, p.key1);
           u = u53((uint64_t)o.x | ((uint64_t)o.y << 32));
         }
         keep = u < p.keep[w];
@@ -269,7 +272,8 @@ __global__ void __launch_bounds__(256) drive_kernel(DriveArgs<T> p) {
           sb.used = 1;
         }
       } else if (p.dynamic) {
-        const uint4 o = philox_tok((uint64_t)(lo_t + koff_s[pos]), (uint32_t)epoch, kTagWin, p.key0, p.key1);
+        const uint4 o = philox_tok((uint64_t)(p.token_base + lo_t + koff_s[pos]),
+                                   p.epoch_base + (uint32_t)epoch, kTagWin, p.key0, p.key1);
         b = 1 + (int)(((uint64_t)o.x * (uint64_t)p.window) >> 32);
       }
       const int wlo = max(pos - b, 0);
@@ -308,7 +312,8 @@ __global__ void __launch_bounds__(256) drive_kernel(DriveArgs<T> p) {
             span = min(32, need + 2);
             if (lane < span) {
               const uint32_t a = attempt + (uint32_t)lane;
-              const uint4 o = philox_tok((uint64_t)(lo_t + koff_s[pos]), (uint32_t)epoch,
+              const uint4 o = philox_tok((uint64_t)(p.token_base + lo_t + koff_s[pos]),
+                                         p.epoch_base + (uint32_t)epoch,
                                          kTagNeg | ((uint32_t)(chunk & 0xFF) << 16) | ((a >> 1) & 0xFFFFu),
                                          p.key0, p.key1);
               const uint32_t bw = (a & 1) ? o.z : o.x, coin = (a & 1) ? o.w : o.y;
@@ -336,6 +341,7 @@ __global__ void __launch_bounds__(256) drive_kernel(DriveArgs<T> p) {
         }
         __syncwarp();
         kc += 1;
+        inputs += mc;
         const bool want = p.loss_every > 0 && (kc % p.loss_every) == 0;
         if (p.trace_cap > 0) {
           int64_t idx = p.trace_count[wid];
@@ -384,6 +390,7 @@ __global__ void __launch_bounds__(256) drive_kernel(DriveArgs<T> p) {
     o.kernel_counter = kc;
     o.words_read = S.words_read + budget_used;
     o.words_trained = S.words_trained + trained;
+    o.inputs = S.inputs + inputs;
   }
 }
 
@@ -593,6 +600,8 @@ static int drive_typed(const sgns_drive_params *p, cudaStream_t st) {
   a.trace_alpha = p->d_trace_alpha;
   a.trace_count = p->d_trace_count;
   a.error = p->d_error;
+  a.token_base = p->token_base;
+  a.epoch_base = (uint32_t)p->epoch_base;
   const int nch = nch_for(a.mv.nvec);
   if (nch < 0) return SGNS_E_SHAPE;
   if (p->rng_mode == SGNS_RNG_SPLITMIX) return drive_typed_rng<T, SGNS_RNG_SPLITMIX>(a, nch, p->warps_per_block, st);
@@ -611,6 +620,13 @@ using namespace sgns;
 extern "C" {
 
 int sgns_abi_version(void) { return SGNS_ABI_VERSION; }
+
+int sgns_struct_sizes(int32_t *worker_bytes, int32_t *params_bytes) {
+  if (!worker_bytes || !params_bytes) return SGNS_E_ARG;
+  *worker_bytes = (int32_t)sizeof(sgns_worker);
+  *params_bytes = (int32_t)sizeof(sgns_drive_params);
+  return SGNS_OK;
+}
 
 const char *sgns_error_string(int32_t code) {
   switch (code) {

@@ -161,3 +161,131 @@ def tiny_config_corpus(seed: int = 0) -> SyntheticCorpus:
 def mid_config_corpus(seed: int = 0) -> SyntheticCorpus:
     """BASELINE.json configs[2]: 17M tokens, Zipf(1.05) over 71k ids."""
     return make_planted_corpus(17_000_000, 71_000, zipf_s=1.05, seed=seed)
+
+
+@dataclass
+class DeviceSyntheticCorpus:
+    """A planted-cluster corpus generated and kept in HBM (configs[3]: 800M tokens)."""
+
+    ids: "object"            # torch int32 (device)
+    offsets: "object"        # torch int64 (device)
+    counts: np.ndarray       # int64 per final id (host)
+    sentence_bytes: np.ndarray
+    clusters: list[np.ndarray]
+    n_tokens: int
+    n_sentences: int
+    max_sentence: int
+
+    def vocabulary(self) -> Vocabulary:
+        return Vocabulary.from_counts(self.counts)
+
+    def host_offsets(self) -> np.ndarray:
+        return self.offsets.cpu().numpy()
+
+    def encoded(self, with_ids: bool = False) -> EncodedCorpus:
+        ids = self.ids.cpu().numpy() if with_ids else np.empty(0, dtype=np.int32)
+        return EncodedCorpus(ids, self.host_offsets(), self.sentence_bytes)
+
+
+def make_planted_corpus_device(
+    n_tokens: int,
+    vocab_size: int,
+    zipf_s: float = 1.05,
+    n_clusters: int = 50,
+    cluster_size: int = 20,
+    sentence_len: int = 50,
+    run_prob: float = 0.5,
+    run_len: int = 8,
+    min_count: int = 5,
+    seed: int = 0,
+    device: str = "cuda",
+    chunk: int = 1 << 26,
+) -> DeviceSyntheticCorpus:
+    """Same construction as make_planted_corpus, generated with torch on the GPU
+    (seeded torch Philox), so 800M-token corpora take seconds instead of minutes.
+    Ids follow the reference vocabulary order (count desc, first occurrence);
+    ids with count < min_count are dropped as encode_corpus drops OOV tokens."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    V = vocab_size
+    ranks = torch.arange(1, V + 1, dtype=torch.float64, device=device)
+    cdf = torch.cumsum(ranks.pow(-zipf_s), 0)
+    cdf /= cdf[-1].clone()
+    raw = torch.empty(n_tokens, dtype=torch.int32, device=device)
+    for lo in range(0, n_tokens, chunk):
+        hi = min(n_tokens, lo + chunk)
+        u = torch.rand(hi - lo, generator=g, dtype=torch.float64, device=device)
+        raw[lo:hi] = torch.searchsorted(cdf, u, right=True).clamp_(max=V - 1).to(torch.int32)
+        del u
+    rng = np.random.default_rng(seed)
+    need = n_clusters * cluster_size
+    band_lo = max(1, V // 50)
+    band_hi = min(max(band_lo + need, V // 5), V)
+    if band_hi - band_lo < need:
+        band_lo, band_hi = 0, V
+    members = rng.choice(np.arange(band_lo, band_hi), size=need, replace=False).astype(np.int32)
+    raw_clusters = members.reshape(n_clusters, cluster_size)
+    n_sent = -(-n_tokens // sentence_len)
+    if n_clusters > 0 and run_len > 0:
+        sel = torch.nonzero(torch.rand(n_sent, generator=g, device=device) < run_prob).flatten()
+        ns = sel.numel()
+        s_lo = sel * sentence_len
+        s_len = torch.clamp(n_tokens - s_lo, max=sentence_len)
+        length = torch.clamp(s_len, max=run_len)
+        start = s_lo + (torch.rand(ns, generator=g, device=device) * (s_len - length + 1)).long()
+        cl = torch.randint(0, n_clusters, (ns,), generator=g, device=device)
+        dev_members = torch.from_numpy(raw_clusters).to(device)
+        for j in range(run_len):
+            ok = j < length
+            pos = (start + j)[ok]
+            pick = torch.randint(0, cluster_size, (ns,), generator=g, device=device)[ok]
+            raw[pos] = dev_members[cl[ok], pick]
+    counts = torch.bincount(raw, minlength=V)
+    first = torch.full((V,), n_tokens, dtype=torch.int64, device=device)
+    for lo in range(0, n_tokens, chunk):
+        hi = min(n_tokens, lo + chunk)
+        first.scatter_reduce_(0, raw[lo:hi].long(),
+                              torch.arange(lo, hi, dtype=torch.int64, device=device), "amin")
+    present = counts >= max(1, min_count)
+    key = torch.where(present, (-counts) * (n_tokens + 1) + first,
+                      torch.full_like(first, torch.iinfo(torch.int64).max))
+    n_present = int(present.sum().item())
+    order = torch.argsort(key)[:n_present]
+    new_id = torch.full((V,), -1, dtype=torch.int32, device=device)
+    new_id[order] = torch.arange(n_present, dtype=torch.int32, device=device)
+    lens = torch.zeros(n_sent, dtype=torch.int64, device=device)
+    sbytes = torch.zeros(n_sent, dtype=torch.float64, device=device)
+    digits = torch.floor(torch.log10(torch.arange(V, device=device, dtype=torch.float64).clamp(min=1))) + 3
+    pieces = []
+    for lo in range(0, n_tokens, chunk):
+        hi = min(n_tokens, lo + chunk)
+        r = raw[lo:hi].long()
+        mapped = new_id[r]
+        keep = mapped >= 0
+        sent = torch.arange(lo, hi, dtype=torch.int64, device=device) // sentence_len
+        lens += torch.bincount(sent[keep], minlength=n_sent)
+        sbytes += torch.bincount(sent, weights=digits[r], minlength=n_sent)
+        pieces.append(mapped[keep])
+        del r, mapped, keep, sent
+    del raw, first
+    ids = torch.cat(pieces)
+    del pieces
+    nonempty = lens > 0
+    lens_ne = lens[nonempty]
+    offsets = torch.zeros(int(lens_ne.numel()) + 1, dtype=torch.int64, device=device)
+    offsets[1:] = torch.cumsum(lens_ne, 0)
+    counts_host = counts[order].cpu().numpy().astype(np.int64)
+    new_host = new_id.cpu().numpy()
+    clusters = [new_host[c][new_host[c] >= 0].astype(np.int64) for c in raw_clusters]
+    return DeviceSyntheticCorpus(ids, offsets, counts_host,
+                                 sbytes[nonempty].cpu().numpy().astype(np.int64), clusters,
+                                 int(ids.numel()), int(lens_ne.numel()),
+                                 int(lens_ne.max().item()) if lens_ne.numel() else 0)
+
+
+def large_config_corpus(seed: int = 0, n_tokens: int = 800_000_000, device: str = "cuda"):
+    """BASELINE.json configs[3]: 800M tokens, Zipf(1.05) over 1M ids, min-count 5."""
+    return make_planted_corpus_device(n_tokens, 1_000_000, zipf_s=1.05, min_count=5, seed=seed,
+                                      device=device)

@@ -42,7 +42,7 @@ _INF_BUDGET = 2**62
 WORKER_DTYPE = np.dtype([
     ("next_sent", "<i8"), ("lo", "<i8"), ("hi", "<i8"), ("epoch", "<i4"), ("done", "<i4"),
     ("rng", "<u8"), ("alpha", "<f8"), ("read_local", "<f8"), ("trained_local", "<f8"),
-    ("kernel_counter", "<i8"), ("words_read", "<i8"), ("words_trained", "<i8")])
+    ("kernel_counter", "<i8"), ("words_read", "<i8"), ("words_trained", "<i8"), ("inputs", "<i8")])
 
 
 class ConfigError(ValueError):
@@ -386,3 +386,118 @@ def train(corpus_path: str, config: TrainingConfig, progress: bool = False):
     encoded = encode_corpus(corpus_path, vocab)
     model, stats = train_encoded(vocab, encoded, config, progress=progress)
     return model, vocab, stats
+
+
+class StreamingTrainer:
+    """Out-of-core training: sentence chunks stream from (pinned) host memory
+    through preallocated HBM buffers while the model, sampler and the shared
+    alpha schedule stay resident.  Each `train_chunk` call is one host->device
+    copy, one driver launch over the chunk (its workers re-split the chunk by
+    tokens), and one tiny device->host read of the chunk's counters.  With
+    rng="philox" the draws are keyed by the global corpus position
+    (`token_base`), so streaming does not change which windows are drawn."""
+
+    def __init__(self, model: DeviceModel, counts: np.ndarray, config: TrainingConfig,
+                 total_x_epochs: float, max_chunk_tokens: int, max_chunk_sentences: int,
+                 max_sentence: int, n_workers: int | None = None, alpha0_eff: float | None = None,
+                 total_tokens: int | None = None, keep_probs: np.ndarray | None = None):
+        torch = _torch()
+        config.validate()
+        if config.rng != "philox":
+            raise ConfigError("streaming training needs rng='philox' (position-keyed draws)")
+        self.torch = torch
+        self.model, self.config = model, config
+        dev = model.m_in.device
+        self.device = dev
+        self.ids = torch.empty(max_chunk_tokens, dtype=torch.int32, device=dev)
+        self.offsets = torch.empty(max_chunk_sentences + 1, dtype=torch.int64, device=dev)
+        self.sampler = DeviceSampler(counts, "philox", device=dev)
+        if keep_probs is None and config.subsample > 0:
+            from .corpus import keep_probabilities
+            keep_probs = keep_probabilities(counts, int(np.sum(counts)), config.subsample)
+        self.keep = None if keep_probs is None else torch.from_numpy(
+            np.ascontiguousarray(keep_probs, dtype=np.float64)).to(dev)
+        if n_workers is None:
+            n_workers = resident_workers(config, max_sentence)
+        self.n_workers = n_workers
+        self.alpha0_eff = config.alpha0 if alpha0_eff is None else alpha0_eff
+        self.total_x_epochs = total_x_epochs
+        self.alpha = self.alpha0_eff
+        self.workers_host = torch.zeros((n_workers * WORKER_DTYPE.itemsize,), dtype=torch.uint8).pin_memory()
+        self.workers = torch.zeros_like(self.workers_host, device=dev)
+        self.shared = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.loss = torch.zeros((n_workers, 1), dtype=torch.float64, device=dev)
+        self.cells = torch.zeros((n_workers, 1), dtype=torch.int64, device=dev)
+        self.stats_dev = torch.zeros(6, dtype=torch.float64, device=dev)
+        self.stats_host = torch.zeros(6, dtype=torch.float64).pin_memory()
+        self.sig = device_sigmoid_table(model.np_dtype, dev)
+        self.max_sentence = max_sentence
+        p = _lib.DriveParams()
+        p.dtype = model.cdtype
+        p.d_m_in, p.d_m_out = model.m_in.data_ptr(), model.m_out.data_ptr()
+        p.vocab, p.ld, p.dim = model.vocab_size, model.ld, model.dim
+        p.d_ids, p.d_offsets = self.ids.data_ptr(), self.offsets.data_ptr()
+        p.d_keep_probs = None if self.keep is None else self.keep.data_ptr()
+        p.rng_mode = _lib.RNG_PHILOX
+        p.d_alias_thr, p.d_alias_idx = self.sampler.alias_thr.data_ptr(), self.sampler.alias_idx.data_ptr()
+        p.seed = config.seed & (2**64 - 1)
+        p.window, p.dynamic, p.k_neg = config.window, int(config.dynamic_window), config.negatives
+        p.batch_cap = config.batch_cap
+        p.sigmoid_mode = _lib.SIGMOID_EXACT if config.float64 else _lib.SIGMOID_TABLE
+        p.d_sig_table = self.sig.data_ptr()
+        p.alpha0, p.floor_frac = self.alpha0_eff, config.alpha_floor_fraction
+        p.total_x_epochs = total_x_epochs
+        p.refresh_words = config.refresh_words
+        p.d_shared = self.shared.data_ptr()
+        p.epochs, p.loss_every = 1, config.loss_sample_every
+        p.d_workers, p.n_workers = self.workers.data_ptr(), n_workers
+        p.d_loss_by_epoch, p.d_cells_by_epoch = self.loss.data_ptr(), self.cells.data_ptr()
+        p.update = 1
+        p.max_sentence = max(max_sentence, 1)
+        p.word_budget = _INF_BUDGET
+        self.params = p
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def train_chunk(self, ids_host, offsets_host: np.ndarray, token_base: int, epoch: int = 0):
+        """Train one chunk; ids_host: pinned torch int32 tensor of the chunk's tokens,
+        offsets_host: int64 sentence offsets of the chunk starting at 0.  Returns the
+        chunk's (words_trained, words_read, loss_sum, loss_cells, inputs, chunks)."""
+        torch = self.torch
+        n_tok = int(offsets_host[-1])
+        n_sent = len(offsets_host) - 1
+        if n_tok > self.ids.numel() or n_sent + 1 > self.offsets.numel():
+            raise ValueError("chunk larger than the streaming buffers")
+        self.ids[:n_tok].copy_(ids_host[:n_tok], non_blocking=True)
+        off_t = torch.from_numpy(np.ascontiguousarray(offsets_host, dtype=np.int64))
+        self.offsets[:n_sent + 1].copy_(off_t, non_blocking=False)
+        ranges = split_by_tokens(offsets_host, 0, n_sent, self.n_workers)
+        w = self.workers_host.numpy().view(WORKER_DTYPE)
+        w[:] = 0
+        w["lo"] = [a for a, _ in ranges]
+        w["next_sent"] = w["lo"]
+        w["hi"] = [b for _, b in ranges]
+        w["alpha"] = self.alpha
+        self.workers.copy_(self.workers_host, non_blocking=True)
+        self.loss.zero_()
+        self.cells.zero_()
+        self.params.token_base = int(token_base)
+        self.params.epoch_base = int(epoch)
+        st = current_stream_ptr(self.device)
+        _lib.check(_lib.lib().sgns_drive(self.params, st), "sgns_drive")
+        wv = self.workers.view(torch.int64).view(self.n_workers, WORKER_DTYPE.itemsize // 8)
+        # int64 columns of sgns_worker: 8 kernel_counter, 9 words_read, 10 words_trained, 11 inputs
+        self.stats_dev[0] = wv[:, 10].sum().double()
+        self.stats_dev[1] = wv[:, 9].sum().double()
+        self.stats_dev[2] = self.loss.sum()
+        self.stats_dev[3] = self.cells.sum().double()
+        self.stats_dev[4] = wv[:, 11].sum().double()
+        self.stats_dev[5] = wv[:, 8].sum().double()
+        self.stats_host.copy_(self.stats_dev, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        s = self.stats_host.numpy()
+        frac = 1.0 - float(self.shared[0].item()) / (self.total_x_epochs + 1.0)
+        self.alpha = self.alpha0_eff * max(frac, self.config.alpha_floor_fraction)
+        self.h2d_bytes = n_tok * 4 + (n_sent + 1) * 8 + self.workers_host.numel()
+        self.d2h_bytes = self.stats_host.numel() * 8 + 8
+        return int(s[0]), int(s[1]), float(s[2]), int(s[3]), int(s[4]), int(s[5])
