@@ -38,7 +38,7 @@ DIM, WINDOW, NEG, SUBSAMPLE, ALPHA0 = 300, 5, 5, 1e-4, 0.025
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--tokens", type=int, default=800_000_000)
@@ -319,7 +319,7 @@ def main():
     achieved = bytes_step / avg_kernel_s / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
-                "kernel": "drive_kernel<float,3,CREG,6,PHILOX>",
+                "kernel": "drive_kernel<float,MODE_F2,NS=5,NCH=3,K1R=6,PHILOX>",
                 "algorithmic_bytes_per_launch": bytes_step,
                 "gflops": flops_step / avg_kernel_s / 1e9,
                 "avg_launch_ms": avg_kernel_s * 1000.0,

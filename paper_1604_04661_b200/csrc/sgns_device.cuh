@@ -374,4 +374,133 @@ __device__ __forceinline__ void window_update(const ModelView<T> &mv, const int 
   __syncwarp();
 }
 
+
+// ------------------------------------------------ float32 fast path (v2) ----
+// Column mapping in 8-byte units: lane l owns float2 slots l + 32 j (j < NS),
+// 150 slots at d = 300 -> 5 slots on 22 lanes, 4 on 10 (94% balanced; the
+// 16-byte mapping wastes 22%).  All arithmetic is packed FFMA2 (Blackwell
+// f32x2), C lives in registers loaded straight from L2, only the m input rows
+// are staged in shared memory (cp.async, 16-byte), and dC is a column-outer
+// pass over the staged rows, so registers stay <= 128 and smem ~12 KB/warp.
+__device__ __forceinline__ float2 f2zero() { return make_float2(0.f, 0.f); }
+__device__ __forceinline__ float2 ld_cg_f2(const float *p) {
+  float2 v;
+  asm volatile("ld.global.cg.v2.f32 {%0, %1}, [%2];\n" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+
+template <int NS, int NCH, int K1R>
+__device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, const int *ids_s, int m,
+                                                 int k1, float alpha, bool exact, const float *sig_s,
+                                                 bool want_loss, double &loss_acc, long long &cell_acc,
+                                                 float *rows_s, float *e_s, int lane) {
+  constexpr int NV = 8;
+  static_assert(K1R <= NV, "K1R <= 8");
+  const int64_t ld = mv.ld;
+  const int nvec = mv.nvec;   // 16-byte chunks per row
+  const int nslot = nvec * 2; // 8-byte slots per row
+
+  // 1. issue the input-row gathers (16-byte cp.async) and the output rows (8-byte
+  //    L2 loads straight into registers) before waiting on either
+  for (int r = 0; r < m; ++r) {
+    const float *src = mv.in_src + (int64_t)ids_s[r] * ld;
+    float *dst = rows_s + (int64_t)r * ld;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) cp_async16(dst + c * 4, src + c * 4);
+    }
+  }
+  float2 c[K1R][NS];
+#pragma unroll
+  for (int k = 0; k < K1R; ++k) {
+    const float *src = mv.out_src + (int64_t)ids_s[m + (k < k1 ? k : 0)] * ld;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const int sl = lane + 32 * j;
+      c[k][j] = (k < k1 && sl < nslot) ? ld_cg_f2(src + 2 * sl) : f2zero();
+    }
+  }
+  cp_async_wait_all();
+  __syncwarp();  // staged rows were copied in 16-byte lanes, read in 8-byte lanes
+
+  const int my_k = reduced_index<NV>(lane);
+  const bool leader = (lane & ((32 / NV) - 1)) == 0;
+  const float2 alpha2 = make_float2(alpha, alpha);
+  for (int i = 0; i < m; ++i) {
+    float2 a[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const int sl = lane + 32 * j;
+      a[j] = sl < nslot ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + 2 * sl) : f2zero();
+    }
+    float p[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      if (k < K1R) {
+        float2 acc = __fmul2_rn(a[0], c[k][0]);
+#pragma unroll
+        for (int j = 1; j < NS; ++j) acc = __ffma2_rn(a[j], c[k][j], acc);
+        p[k] = acc.x + acc.y;
+      } else {
+        p[k] = 0.f;
+      }
+    }
+    const float s = transpose_reduce<NV>(p, lane);
+    float er = 0.f, es = 0.f;
+    if (my_k < k1) {
+      cell_error<float>(s, my_k, alpha, exact, sig_s, er, es);
+      if (leader) {
+        e_s[i * k1 + my_k] = es;
+        if (want_loss) {
+          loss_acc += softplus(my_k == 0 ? -(double)s : (double)s);
+          cell_acc += 1;
+        }
+      }
+    }
+    // dA_i = alpha * sum_k err_ik C_k   (kernel_batched.py:201-210)
+    float2 d[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) d[j] = f2zero();
+#pragma unroll
+    for (int k = 0; k < K1R; ++k) {
+      const float ek = __shfl_sync(0xffffffffu, er, group_leader<NV>(k));
+      const float2 ek2 = make_float2(ek, ek);
+#pragma unroll
+      for (int j = 0; j < NS; ++j) d[j] = __ffma2_rn(ek2, c[k][j], d[j]);
+    }
+    float *dst = mv.in_dst + (int64_t)ids_s[i] * ld;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const int sl = lane + 32 * j;
+      if (sl < nslot) atomicAdd(reinterpret_cast<float2 *>(dst + 2 * sl), __fmul2_rn(d[j], alpha2));
+    }
+  }
+  __syncwarp();
+  // dC_k = sum_i (alpha err_ik) A_i, column-outer over the staged rows
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+    const int sl = lane + 32 * j;
+    if (sl >= nslot) continue;
+    float2 acc[K1R];
+#pragma unroll
+    for (int k = 0; k < K1R; ++k) acc[k] = f2zero();
+    for (int i = 0; i < m; ++i) {
+      const float2 a = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + 2 * sl);
+#pragma unroll
+      for (int k = 0; k < K1R; ++k) {
+        if (k < k1) {
+          const float e = e_s[i * k1 + k];
+          acc[k] = __ffma2_rn(make_float2(e, e), a, acc[k]);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K1R; ++k)
+      if (k < k1)
+        atomicAdd(reinterpret_cast<float2 *>(mv.out_dst + (int64_t)ids_s[m + k] * ld + 2 * sl), acc[k]);
+  }
+  __syncwarp();
+}
+
 }  // namespace sgns

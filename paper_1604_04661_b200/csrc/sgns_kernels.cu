@@ -28,10 +28,13 @@ __host__ __device__ inline int64_t round16(int64_t b) { return (b + 15) & ~int64
 struct Slab {
   int64_t rows, e, ids, kept, off, total;
 };
-__host__ __device__ inline Slab slab_layout(int64_t elem, int64_t ld, int mcap, int k1, int kept_cap) {
+// MODE_F2: float32 fast path (only the m input rows are staged); MODE_SMEM: all rows staged
+enum { MODE_SMEM = 0, MODE_F2 = 1 };
+__host__ __device__ inline Slab slab_layout(int mode, int64_t elem, int64_t ld, int mcap, int k1,
+                                            int kept_cap) {
   Slab s;
   s.rows = 0;
-  s.e = round16((int64_t)(mcap + k1) * ld * elem);
+  s.e = round16((int64_t)(mode == MODE_F2 ? mcap : mcap + k1) * ld * elem);
   s.ids = s.e + round16((int64_t)2 * mcap * k1 * elem);
   s.kept = s.ids + round16((int64_t)(mcap + k1) * 4);
   s.off = s.kept + round16((int64_t)kept_cap * 4);
@@ -65,6 +68,20 @@ __device__ __forceinline__ void flush_loss(double loss, long long cells, double 
   }
 }
 
+template <typename T, int MODE, int NS, int NCH, int K1R>
+__device__ __forceinline__ void run_window(const ModelView<T> &mv, const int *ids_s, int m, int k1,
+                                           T alpha, bool exact, const T *sig_s, bool want,
+                                           double &loss, long long &cells, T *rows_s, T *e_s,
+                                           int lane) {
+  if constexpr (MODE == MODE_F2) {
+    window_update_f2<NS, NCH, K1R>(mv, ids_s, m, k1, alpha, exact, sig_s, want, loss, cells,
+                                   rows_s, e_s, lane);
+  } else {
+    window_update<T, NCH, false, 0>(mv, ids_s, m, k1, alpha, exact, sig_s, want, loss, cells,
+                                    rows_s, e_s, lane);
+  }
+}
+
 // ------------------------------------------------------- update_windows ----
 template <typename T> struct UpdateArgs {
   ModelView<T> mv;
@@ -78,13 +95,13 @@ template <typename T> struct UpdateArgs {
   int wpb;
 };
 
-template <typename T, int NCH, bool CREG, int K1R>
-__global__ void __launch_bounds__(256) update_windows_kernel(UpdateArgs<T> p) {
+template <typename T, int MODE, int NS, int NCH, int K1R>
+__global__ void __launch_bounds__(256, MODE == MODE_F2 ? 2 : 1) update_windows_kernel(UpdateArgs<T> p) {
   extern __shared__ __align__(16) unsigned char smem[];
   T *sig_s = reinterpret_cast<T *>(smem);
   load_table(sig_s, p.sig);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Slab L = slab_layout(sizeof(T), p.mv.ld, p.mcap, p.k1, 0);
+  const Slab L = slab_layout(MODE, sizeof(T), p.mv.ld, p.mcap, p.k1, 0);
   unsigned char *base = smem + table_bytes(sizeof(T)) + (int64_t)warp * L.total;
   T *rows_s = reinterpret_cast<T *>(base + L.rows);
   T *e_s = reinterpret_cast<T *>(base + L.e);
@@ -102,8 +119,8 @@ __global__ void __launch_bounds__(256) update_windows_kernel(UpdateArgs<T> p) {
       ids_s[r] = r < m ? p.in_ids[lo + r] : p.out_ids[(int64_t)w * p.k1 + (r - m)];
     __syncwarp();
     const bool want = p.loss_every > 0 && (w % p.loss_every) == 0;
-    window_update<T, NCH, CREG, K1R>(p.mv, ids_s, m, p.k1, p.alpha[w], p.exact != 0, sig_s, want,
-                                     loss, cells, rows_s, e_s, lane);
+    run_window<T, MODE, NS, NCH, K1R>(p.mv, ids_s, m, p.k1, p.alpha[w], p.exact != 0, sig_s, want,
+                                      loss, cells, rows_s, e_s, lane);
   }
   if (p.loss_every > 0) flush_loss<T>(loss, cells, p.loss_sum, p.loss_cells, true, lane);
 }
@@ -156,8 +173,8 @@ struct SmBatch {
   __device__ __forceinline__ uint64_t state_after() const { return base + (uint64_t)used * kGolden; }
 };
 
-template <typename T, int NCH, bool CREG, int K1R, int RNG>
-__global__ void __launch_bounds__(256) drive_kernel(DriveArgs<T> p) {
+template <typename T, int MODE, int NS, int NCH, int K1R, int RNG>
+__global__ void __launch_bounds__(256, MODE == MODE_F2 ? 2 : 1) drive_kernel(DriveArgs<T> p) {
   extern __shared__ __align__(16) unsigned char smem[];
   T *sig_s = reinterpret_cast<T *>(smem);
   load_table(sig_s, p.sig);
@@ -166,7 +183,7 @@ __global__ void __launch_bounds__(256) drive_kernel(DriveArgs<T> p) {
   if (wid >= p.n_workers) return;
   const int k1 = p.k_neg + 1;
   const int mcap = min(p.cap, 2 * p.window);
-  const Slab L = slab_layout(sizeof(T), p.mv.ld, mcap, k1, p.kept_cap);
+  const Slab L = slab_layout(MODE, sizeof(T), p.mv.ld, mcap, k1, p.kept_cap);
   unsigned char *base = smem + table_bytes(sizeof(T)) + (int64_t)warp * L.total;
   T *rows_s = reinterpret_cast<T *>(base + L.rows);
   T *e_s = reinterpret_cast<T *>(base + L.e);
@@ -363,8 +380,8 @@ __global__ void __launch_bounds__(256) drive_kernel(DriveArgs<T> p) {
           if (lane == 0) p.trace_count[wid] = idx + 1;
         }
         if (p.update)
-          window_update<T, NCH, CREG, K1R>(p.mv, ids_s, mc, k1, alpha_t, p.exact != 0, sig_s, want,
-                                           loss, cells, rows_s, e_s, lane);
+          run_window<T, MODE, NS, NCH, K1R>(p.mv, ids_s, mc, k1, alpha_t, p.exact != 0, sig_s, want,
+                                            loss, cells, rows_s, e_s, lane);
         __syncwarp();
       }
       if (RNG == SGNS_RNG_SPLITMIX) rng = sb.state_after();
@@ -480,29 +497,34 @@ static int choose_wpb(K kernel, int64_t table, int64_t slab, int *wpb_out, int *
   return 0;
 }
 
-template <typename T, int NCH, bool CREG, int K1R>
+template <typename T, int MODE, int NS, int NCH, int K1R>
 static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
-  auto kern = update_windows_kernel<T, NCH, CREG, K1R>;
-  const Slab L = slab_layout(sizeof(T), a.mv.ld, a.mcap, a.k1, 0);
+  auto kern = update_windows_kernel<T, MODE, NS, NCH, K1R>;
+  const Slab L = slab_layout(MODE, sizeof(T), a.mv.ld, a.mcap, a.k1, 0);
   int wpb = 0, bps = 0;
   int rc = choose_wpb(kern, table_bytes(sizeof(T)), L.total, &wpb, &bps);
   if (rc) return rc;
   a.wpb = wpb;
   const int64_t bytes = table_bytes(sizeof(T)) + (int64_t)wpb * L.total;
+  if ((rc = prepare(kern, bytes))) return rc;
   const int64_t blocks_needed = (a.n_win + wpb - 1) / wpb;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)num_sms() * bps));
   kern<<<grid, wpb * 32, bytes, st>>>(a);
   return (int)cudaGetLastError();
 }
 
-template <typename T, int NCH, bool CREG, int K1R, int RNG>
-static int launch_drive_t(DriveArgs<T> a, int wpb_req, cudaStream_t st) {
-  auto kern = drive_kernel<T, NCH, CREG, K1R, RNG>;
+template <typename T, int MODE, int NS, int NCH, int K1R, int RNG>
+static int launch_drive_t(DriveArgs<T> a, int wpb_req, cudaStream_t st, int *resident = nullptr) {
+  auto kern = drive_kernel<T, MODE, NS, NCH, K1R, RNG>;
   const int k1 = a.k_neg + 1;
-  const Slab L = slab_layout(sizeof(T), a.mv.ld, std::min(a.cap, 2 * a.window), k1, a.kept_cap);
+  const Slab L = slab_layout(MODE, sizeof(T), a.mv.ld, std::min(a.cap, 2 * a.window), k1, a.kept_cap);
   int wpb = 0, bps = 0;
   int rc = choose_wpb(kern, table_bytes(sizeof(T)), L.total, &wpb, &bps);
   if (rc) return rc;
+  if (resident) {  // occupancy query only
+    *resident = wpb * bps * num_sms();
+    return 0;
+  }
   if (wpb_req > 0) wpb = wpb_req;
   a.wpb = wpb;
   const int64_t bytes = table_bytes(sizeof(T)) + (int64_t)wpb * L.total;
@@ -512,56 +534,97 @@ static int launch_drive_t(DriveArgs<T> a, int wpb_req, cudaStream_t st) {
   return (int)cudaGetLastError();
 }
 
-template <typename T, int NCH>
-static int dispatch_update(UpdateArgs<T> a, cudaStream_t st) {
-  if constexpr (sizeof(T) == 4 && NCH <= 4) {
-    if (a.k1 <= 6) return launch_update_t<T, NCH, true, 6>(a, st);
-  }
-  if constexpr (sizeof(T) == 4 && NCH <= 3) {
-    if (a.k1 <= 8) return launch_update_t<T, NCH, true, 8>(a, st);
-  }
-  return launch_update_t<T, NCH, false, 0>(a, st);
+// float32 fast path: k1 <= 8 and d <= 512 (NS = float2 slots per lane)
+static int ns_for(int64_t ld_elems_f32) { return (int)((ld_elems_f32 / 2 + 31) / 32); }
+
+template <int NS, int RNG>
+static int drive_f2(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
+  constexpr int NCH = (NS + 1) / 2;
+  if (a.k_neg + 1 <= 6) return launch_drive_t<float, MODE_F2, NS, NCH, 6, RNG>(a, wpb, st, res);
+  return launch_drive_t<float, MODE_F2, NS, NCH, 8, RNG>(a, wpb, st, res);
 }
 
-template <typename T, int NCH, int RNG>
-static int dispatch_drive(DriveArgs<T> a, int wpb, cudaStream_t st) {
-  const int k1 = a.k_neg + 1;
-  if constexpr (sizeof(T) == 4 && NCH <= 4) {
-    if (k1 <= 6) return launch_drive_t<T, NCH, true, 6, RNG>(a, wpb, st);
+template <int RNG>
+static int drive_f32(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
+  const int ns = ns_for(a.mv.ld);
+  if (a.k_neg + 1 <= 8) {
+    switch (ns) {
+      case 1: return drive_f2<1, RNG>(a, wpb, st, res);
+      case 2: return drive_f2<2, RNG>(a, wpb, st, res);
+      case 3: return drive_f2<3, RNG>(a, wpb, st, res);
+      case 4: return drive_f2<4, RNG>(a, wpb, st, res);
+      case 5: return drive_f2<5, RNG>(a, wpb, st, res);
+      case 6: return drive_f2<6, RNG>(a, wpb, st, res);
+      case 7: return drive_f2<7, RNG>(a, wpb, st, res);
+      case 8: return drive_f2<8, RNG>(a, wpb, st, res);
+    }
   }
-  if constexpr (sizeof(T) == 4 && NCH <= 3) {
-    if (k1 <= 8) return launch_drive_t<T, NCH, true, 8, RNG>(a, wpb, st);
-  }
-  return launch_drive_t<T, NCH, false, 0, RNG>(a, wpb, st);
-}
-
-template <typename T>
-static int update_typed(UpdateArgs<T> a, int nch, cudaStream_t st) {
-  switch (nch) {
-    case 1: return dispatch_update<T, 1>(a, st);
-    case 2: return dispatch_update<T, 2>(a, st);
-    case 3: return dispatch_update<T, 3>(a, st);
-    case 4: return dispatch_update<T, 4>(a, st);
-    case 8: return dispatch_update<T, 8>(a, st);
+  switch (nch_for(a.mv.nvec)) {
+    case 1: return launch_drive_t<float, MODE_SMEM, 0, 1, 0, RNG>(a, wpb, st, res);
+    case 2: return launch_drive_t<float, MODE_SMEM, 0, 2, 0, RNG>(a, wpb, st, res);
+    case 3: return launch_drive_t<float, MODE_SMEM, 0, 3, 0, RNG>(a, wpb, st, res);
+    case 4: return launch_drive_t<float, MODE_SMEM, 0, 4, 0, RNG>(a, wpb, st, res);
+    case 8: return launch_drive_t<float, MODE_SMEM, 0, 8, 0, RNG>(a, wpb, st, res);
   }
   return SGNS_E_SHAPE;
 }
 
-template <typename T, int RNG>
-static int drive_typed_rng(DriveArgs<T> a, int nch, int wpb, cudaStream_t st) {
-  switch (nch) {
-    case 1: return dispatch_drive<T, 1, RNG>(a, wpb, st);
-    case 2: return dispatch_drive<T, 2, RNG>(a, wpb, st);
-    case 3: return dispatch_drive<T, 3, RNG>(a, wpb, st);
-    case 4: return dispatch_drive<T, 4, RNG>(a, wpb, st);
-    case 8: return dispatch_drive<T, 8, RNG>(a, wpb, st);
+template <int RNG>
+static int drive_f64(DriveArgs<double> a, int wpb, cudaStream_t st, int *res) {
+  switch (nch_for(a.mv.nvec)) {
+    case 1: return launch_drive_t<double, MODE_SMEM, 0, 1, 0, RNG>(a, wpb, st, res);
+    case 2: return launch_drive_t<double, MODE_SMEM, 0, 2, 0, RNG>(a, wpb, st, res);
+    case 3: return launch_drive_t<double, MODE_SMEM, 0, 3, 0, RNG>(a, wpb, st, res);
+    case 4: return launch_drive_t<double, MODE_SMEM, 0, 4, 0, RNG>(a, wpb, st, res);
+    case 8: return launch_drive_t<double, MODE_SMEM, 0, 8, 0, RNG>(a, wpb, st, res);
+  }
+  return SGNS_E_SHAPE;
+}
+
+template <int NS>
+static int update_f2(UpdateArgs<float> a, cudaStream_t st) {
+  constexpr int NCH = (NS + 1) / 2;
+  if (a.k1 <= 6) return launch_update_t<float, MODE_F2, NS, NCH, 6>(a, st);
+  return launch_update_t<float, MODE_F2, NS, NCH, 8>(a, st);
+}
+
+static int update_f32(UpdateArgs<float> a, cudaStream_t st) {
+  const int ns = ns_for(a.mv.ld);
+  if (a.k1 <= 8) {
+    switch (ns) {
+      case 1: return update_f2<1>(a, st);
+      case 2: return update_f2<2>(a, st);
+      case 3: return update_f2<3>(a, st);
+      case 4: return update_f2<4>(a, st);
+      case 5: return update_f2<5>(a, st);
+      case 6: return update_f2<6>(a, st);
+      case 7: return update_f2<7>(a, st);
+      case 8: return update_f2<8>(a, st);
+    }
+  }
+  switch (nch_for(a.mv.nvec)) {
+    case 1: return launch_update_t<float, MODE_SMEM, 0, 1, 0>(a, st);
+    case 2: return launch_update_t<float, MODE_SMEM, 0, 2, 0>(a, st);
+    case 3: return launch_update_t<float, MODE_SMEM, 0, 3, 0>(a, st);
+    case 4: return launch_update_t<float, MODE_SMEM, 0, 4, 0>(a, st);
+    case 8: return launch_update_t<float, MODE_SMEM, 0, 8, 0>(a, st);
+  }
+  return SGNS_E_SHAPE;
+}
+
+static int update_f64(UpdateArgs<double> a, cudaStream_t st) {
+  switch (nch_for(a.mv.nvec)) {
+    case 1: return launch_update_t<double, MODE_SMEM, 0, 1, 0>(a, st);
+    case 2: return launch_update_t<double, MODE_SMEM, 0, 2, 0>(a, st);
+    case 3: return launch_update_t<double, MODE_SMEM, 0, 3, 0>(a, st);
+    case 4: return launch_update_t<double, MODE_SMEM, 0, 4, 0>(a, st);
+    case 8: return launch_update_t<double, MODE_SMEM, 0, 8, 0>(a, st);
   }
   return SGNS_E_SHAPE;
 }
 
 template <typename T>
-static int drive_typed(const sgns_drive_params *p, cudaStream_t st) {
-  DriveArgs<T> a;
+static void fill_drive_args(DriveArgs<T> &a, const sgns_drive_params *p) {
   std::memset(&a, 0, sizeof(a));
   T *mi = static_cast<T *>(p->d_m_in), *mo = static_cast<T *>(p->d_m_out);
   a.mv = ModelView<T>{mi, mo, mi, mo, p->ld, (int)(p->ld * (int64_t)sizeof(T) / 16)};
@@ -602,10 +665,22 @@ static int drive_typed(const sgns_drive_params *p, cudaStream_t st) {
   a.error = p->d_error;
   a.token_base = p->token_base;
   a.epoch_base = (uint32_t)p->epoch_base;
-  const int nch = nch_for(a.mv.nvec);
-  if (nch < 0) return SGNS_E_SHAPE;
-  if (p->rng_mode == SGNS_RNG_SPLITMIX) return drive_typed_rng<T, SGNS_RNG_SPLITMIX>(a, nch, p->warps_per_block, st);
-  return drive_typed_rng<T, SGNS_RNG_PHILOX>(a, nch, p->warps_per_block, st);
+}
+
+static int drive_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
+  const int wpb = p->warps_per_block;
+  if (p->dtype == SGNS_F32) {
+    DriveArgs<float> a;
+    fill_drive_args(a, p);
+    if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
+    return p->rng_mode == SGNS_RNG_SPLITMIX ? drive_f32<SGNS_RNG_SPLITMIX>(a, wpb, st, resident)
+                                            : drive_f32<SGNS_RNG_PHILOX>(a, wpb, st, resident);
+  }
+  DriveArgs<double> a;
+  fill_drive_args(a, p);
+  if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
+  return p->rng_mode == SGNS_RNG_SPLITMIX ? drive_f64<SGNS_RNG_SPLITMIX>(a, wpb, st, resident)
+                                          : drive_f64<SGNS_RNG_PHILOX>(a, wpb, st, resident);
 }
 
 static bool ld_ok(int32_t dtype, int32_t dim, int64_t ld) {
@@ -666,7 +741,8 @@ int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, cons
     a.exact = sigmoid_mode == SGNS_SIGMOID_EXACT;
     a.loss_every = loss_every; a.loss_sum = d_loss_sum; a.loss_cells = d_loss_cells;
     a.error = d_error; a.wpb = 1;
-    return update_typed<float>(a, nch_for(a.mv.nvec), st);
+    if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
+    return update_f32(a, st);
   }
   if (dtype == SGNS_F64) {
     UpdateArgs<double> a;
@@ -680,7 +756,8 @@ int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, cons
     a.exact = sigmoid_mode == SGNS_SIGMOID_EXACT;
     a.loss_every = loss_every; a.loss_sum = d_loss_sum; a.loss_cells = d_loss_cells;
     a.error = d_error; a.wpb = 1;
-    return update_typed<double>(a, nch_for(a.mv.nvec), st);
+    if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
+    return update_f64(a, st);
   }
   return SGNS_E_ARG;
 }
@@ -698,10 +775,8 @@ int sgns_drive(const sgns_drive_params *p, void *stream) {
   if (p->rng_mode == SGNS_RNG_PHILOX && (!p->d_alias_thr || !p->d_alias_idx)) return SGNS_E_ARG;
   if (p->rng_mode != SGNS_RNG_SPLITMIX && p->rng_mode != SGNS_RNG_PHILOX) return SGNS_E_ARG;
   if (p->trace_cap > 0 && (!p->d_trace || !p->d_trace_alpha || !p->d_trace_count)) return SGNS_E_ARG;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (p->dtype == SGNS_F32) return drive_typed<float>(p, st);
-  if (p->dtype == SGNS_F64) return drive_typed<double>(p, st);
-  return SGNS_E_ARG;
+  if (p->dtype != SGNS_F32 && p->dtype != SGNS_F64) return SGNS_E_ARG;
+  return drive_dispatch(p, static_cast<cudaStream_t>(stream), nullptr);
 }
 
 int sgns_init_model(int32_t dtype, void *d_m_in, void *d_m_out, int64_t vocab, int32_t dim,
@@ -738,30 +813,23 @@ int sgns_expand_slots(const int64_t *d_boundaries, int64_t vocab, int32_t *d_slo
 
 int sgns_resident_workers(int32_t dtype, int32_t dim, int32_t window, int32_t k_neg, int32_t batch_cap,
                           int32_t max_sentence, int32_t *out_workers) {
-  if (!out_workers) return SGNS_E_ARG;
+  if (!out_workers || dim < 1 || window < 1 || k_neg < 1 || batch_cap < 1) return SGNS_E_ARG;
+  if (k_neg + 1 > kMaxK1) return SGNS_E_SHAPE;
+  sgns_drive_params p;
+  std::memset(&p, 0, sizeof(p));
   const int64_t elem = dtype == SGNS_F64 ? 8 : 4;
-  const int64_t ld = ((dim * elem + 15) / 16) * 16 / elem;
-  const int nch = nch_for((int)(ld * elem / 16));
-  if (nch < 0 || k_neg + 1 > kMaxK1) return SGNS_E_SHAPE;
-  const int k1 = k_neg + 1;
-  const int kept = ((std::max(max_sentence, 1) + 31) / 32) * 32;
-  const Slab L = slab_layout(elem, ld, std::min(batch_cap, 2 * window), k1, kept);
-  int wpb = 0, bps = 0, rc;
-  // occupancy of the kernel this configuration dispatches to (registers + smem)
-  if (dtype == SGNS_F32 && nch <= 4 && k1 <= 6) {
-    switch (nch) {
-      case 1: rc = choose_wpb(drive_kernel<float, 1, true, 6, SGNS_RNG_PHILOX>, table_bytes(elem), L.total, &wpb, &bps); break;
-      case 2: rc = choose_wpb(drive_kernel<float, 2, true, 6, SGNS_RNG_PHILOX>, table_bytes(elem), L.total, &wpb, &bps); break;
-      case 3: rc = choose_wpb(drive_kernel<float, 3, true, 6, SGNS_RNG_PHILOX>, table_bytes(elem), L.total, &wpb, &bps); break;
-      default: rc = choose_wpb(drive_kernel<float, 4, true, 6, SGNS_RNG_PHILOX>, table_bytes(elem), L.total, &wpb, &bps); break;
-    }
-  } else if (dtype == SGNS_F32) {
-    rc = choose_wpb(drive_kernel<float, 8, false, 0, SGNS_RNG_PHILOX>, table_bytes(elem), L.total, &wpb, &bps);
-  } else {
-    rc = choose_wpb(drive_kernel<double, 8, false, 0, SGNS_RNG_PHILOX>, table_bytes(elem), L.total, &wpb, &bps);
-  }
+  p.dtype = dtype;
+  p.ld = ((dim * elem + 15) / 16) * 16 / elem;
+  p.dim = dim;
+  p.window = window;
+  p.k_neg = k_neg;
+  p.batch_cap = batch_cap;
+  p.max_sentence = max_sentence;
+  p.rng_mode = SGNS_RNG_PHILOX;
+  int resident = 0;
+  const int rc = drive_dispatch(&p, nullptr, &resident);
   if (rc) return rc;
-  *out_workers = wpb * bps * num_sms();
+  *out_workers = resident;
   return SGNS_OK;
 }
 
