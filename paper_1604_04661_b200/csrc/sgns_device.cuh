@@ -389,37 +389,38 @@ __device__ __forceinline__ float2 ld_cg_f2(const float *p) {
   return v;
 }
 
-template <int NS, int NCH, int K1R>
-__device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, const int *ids_s, int m,
-                                                 int k1, float alpha, bool exact, const float *sig_s,
-                                                 bool want_loss, double &loss_acc, long long &cell_acc,
+template <int NS, int NCH, int K1R, bool EXACT_K>
+__device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, const uint32_t *off_s,
+                                                 int m, int k1, float alpha, bool exact,
+                                                 const float *sig_s, bool want_loss,
+                                                 double &loss_acc, long long &cell_acc,
                                                  float *rows_s, float *e_s, int lane) {
   constexpr int NV = 8;
   static_assert(K1R <= NV, "K1R <= 8");
+  if constexpr (EXACT_K) k1 = K1R;
   const int64_t ld = mv.ld;
-  const int nvec = mv.nvec;   // 16-byte chunks per row
-  const int nslot = nvec * 2; // 8-byte slots per row
+  const int nvec = mv.nvec;    // 16-byte chunks per row
+  const int nslot = nvec * 2;  // 8-byte slots per row
+  // slot j of this lane is always in range for j < NS - 1 (NS = ceil(nslot / 32))
+  auto slot_ok = [&](int j) { return j < NS - 1 || lane + 32 * j < nslot; };
+  auto chunk_ok = [&](int j) { return j < NCH - 1 || lane + 32 * j < nvec; };
+  auto kk_ok = [&](int k) { return EXACT_K || k < k1; };
 
-  // 1. issue the input-row gathers (16-byte cp.async) and the output rows (8-byte
-  //    L2 loads straight into registers) before waiting on either
+  // 1. gathers: input rows -> smem (16-byte cp.async), output rows -> registers (8-byte L2 loads)
   for (int r = 0; r < m; ++r) {
-    const float *src = mv.in_src + (int64_t)ids_s[r] * ld;
+    const float *src = mv.in_src + off_s[r];
     float *dst = rows_s + (int64_t)r * ld;
 #pragma unroll
-    for (int j = 0; j < NCH; ++j) {
-      const int c = lane + 32 * j;
-      if (c < nvec) cp_async16(dst + c * 4, src + c * 4);
-    }
+    for (int j = 0; j < NCH; ++j)
+      if (chunk_ok(j)) cp_async16(dst + (lane + 32 * j) * 4, src + (lane + 32 * j) * 4);
   }
   float2 c[K1R][NS];
 #pragma unroll
   for (int k = 0; k < K1R; ++k) {
-    const float *src = mv.out_src + (int64_t)ids_s[m + (k < k1 ? k : 0)] * ld;
+    const float *src = mv.out_src + off_s[m + (kk_ok(k) ? k : 0)];
 #pragma unroll
-    for (int j = 0; j < NS; ++j) {
-      const int sl = lane + 32 * j;
-      c[k][j] = (k < k1 && sl < nslot) ? ld_cg_f2(src + 2 * sl) : f2zero();
-    }
+    for (int j = 0; j < NS; ++j)
+      c[k][j] = (kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 2 * (lane + 32 * j)) : f2zero();
   }
   cp_async_wait_all();
   __syncwarp();  // staged rows were copied in 16-byte lanes, read in 8-byte lanes
@@ -430,10 +431,9 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
   for (int i = 0; i < m; ++i) {
     float2 a[NS];
 #pragma unroll
-    for (int j = 0; j < NS; ++j) {
-      const int sl = lane + 32 * j;
-      a[j] = sl < nslot ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + 2 * sl) : f2zero();
-    }
+    for (int j = 0; j < NS; ++j)
+      a[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + 2 * (lane + 32 * j))
+                        : f2zero();
     float p[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
@@ -451,7 +451,7 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
     if (my_k < k1) {
       cell_error<float>(s, my_k, alpha, exact, sig_s, er, es);
       if (leader) {
-        e_s[i * k1 + my_k] = es;
+        e_s[i * K1R + my_k] = es;
         if (want_loss) {
           loss_acc += softplus(my_k == 0 ? -(double)s : (double)s);
           cell_acc += 1;
@@ -461,44 +461,52 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
     // dA_i = alpha * sum_k err_ik C_k   (kernel_batched.py:201-210)
     float2 d[NS];
 #pragma unroll
-    for (int j = 0; j < NS; ++j) d[j] = f2zero();
-#pragma unroll
     for (int k = 0; k < K1R; ++k) {
       const float ek = __shfl_sync(0xffffffffu, er, group_leader<NV>(k));
       const float2 ek2 = make_float2(ek, ek);
 #pragma unroll
-      for (int j = 0; j < NS; ++j) d[j] = __ffma2_rn(ek2, c[k][j], d[j]);
+      for (int j = 0; j < NS; ++j) d[j] = k == 0 ? __fmul2_rn(ek2, c[0][j]) : __ffma2_rn(ek2, c[k][j], d[j]);
     }
-    float *dst = mv.in_dst + (int64_t)ids_s[i] * ld;
+    float *dst = mv.in_dst + off_s[i];
 #pragma unroll
-    for (int j = 0; j < NS; ++j) {
-      const int sl = lane + 32 * j;
-      if (sl < nslot) atomicAdd(reinterpret_cast<float2 *>(dst + 2 * sl), __fmul2_rn(d[j], alpha2));
-    }
+    for (int j = 0; j < NS; ++j)
+      if (slot_ok(j))
+        atomicAdd(reinterpret_cast<float2 *>(dst + 2 * (lane + 32 * j)), __fmul2_rn(d[j], alpha2));
   }
   __syncwarp();
-  // dC_k = sum_i (alpha err_ik) A_i, column-outer over the staged rows
+  // dC_k = sum_i (alpha err_ik) A_i, column-outer over the staged rows (i unrolled by 2)
 #pragma unroll
   for (int j = 0; j < NS; ++j) {
-    const int sl = lane + 32 * j;
-    if (sl >= nslot) continue;
+    if (!slot_ok(j)) continue;
+    const int col = 2 * (lane + 32 * j);
     float2 acc[K1R];
 #pragma unroll
     for (int k = 0; k < K1R; ++k) acc[k] = f2zero();
-    for (int i = 0; i < m; ++i) {
-      const float2 a = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + 2 * sl);
+    int i = 0;
+    for (; i + 1 < m; i += 2) {
+      const float2 a0 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col);
+      const float2 a1 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)(i + 1) * ld + col);
 #pragma unroll
       for (int k = 0; k < K1R; ++k) {
-        if (k < k1) {
-          const float e = e_s[i * k1 + k];
-          acc[k] = __ffma2_rn(make_float2(e, e), a, acc[k]);
+        if (kk_ok(k)) {
+          const float e0 = e_s[i * K1R + k], e1 = e_s[(i + 1) * K1R + k];
+          acc[k] = __ffma2_rn(make_float2(e0, e0), a0, acc[k]);
+          acc[k] = __ffma2_rn(make_float2(e1, e1), a1, acc[k]);
         }
       }
     }
+    if (i < m) {
+      const float2 a0 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col);
+#pragma unroll
+      for (int k = 0; k < K1R; ++k)
+        if (kk_ok(k)) {
+          const float e0 = e_s[i * K1R + k];
+          acc[k] = __ffma2_rn(make_float2(e0, e0), a0, acc[k]);
+        }
+    }
 #pragma unroll
     for (int k = 0; k < K1R; ++k)
-      if (k < k1)
-        atomicAdd(reinterpret_cast<float2 *>(mv.out_dst + (int64_t)ids_s[m + k] * ld + 2 * sl), acc[k]);
+      if (kk_ok(k)) atomicAdd(reinterpret_cast<float2 *>(mv.out_dst + off_s[m + k] + col), acc[k]);
   }
   __syncwarp();
 }

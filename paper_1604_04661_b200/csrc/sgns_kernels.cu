@@ -26,7 +26,7 @@ __host__ __device__ inline int64_t round16(int64_t b) { return (b + 15) & ~int64
 
 // shared-memory slab of one warp
 struct Slab {
-  int64_t rows, e, ids, kept, off, total;
+  int64_t rows, e, ids, roff, kept, off, total;
 };
 // MODE_F2: float32 fast path (only the m input rows are staged); MODE_SMEM: all rows staged
 enum { MODE_SMEM = 0, MODE_F2 = 1 };
@@ -36,7 +36,8 @@ __host__ __device__ inline Slab slab_layout(int mode, int64_t elem, int64_t ld, 
   s.rows = 0;
   s.e = round16((int64_t)(mode == MODE_F2 ? mcap : mcap + k1) * ld * elem);
   s.ids = s.e + round16((int64_t)2 * mcap * k1 * elem);
-  s.kept = s.ids + round16((int64_t)(mcap + k1) * 4);
+  s.roff = s.ids + round16((int64_t)(mcap + k1) * 4);
+  s.kept = s.roff + round16((int64_t)(mcap + k1) * 4);
   s.off = s.kept + round16((int64_t)kept_cap * 4);
   s.total = s.off + round16((int64_t)kept_cap * 4);
   return s;
@@ -68,14 +69,18 @@ __device__ __forceinline__ void flush_loss(double loss, long long cells, double 
   }
 }
 
+// K1R == 6 is instantiated for k1 == 6 exactly (K = 5, the north-star shape); K1R == 8
+// covers k1 <= 8 with predicates.
 template <typename T, int MODE, int NS, int NCH, int K1R>
-__device__ __forceinline__ void run_window(const ModelView<T> &mv, const int *ids_s, int m, int k1,
-                                           T alpha, bool exact, const T *sig_s, bool want,
-                                           double &loss, long long &cells, T *rows_s, T *e_s,
-                                           int lane) {
+__device__ __forceinline__ void run_window(const ModelView<T> &mv, const int *ids_s, uint32_t *roff_s,
+                                           int m, int k1, T alpha, bool exact, const T *sig_s,
+                                           bool want, double &loss, long long &cells, T *rows_s,
+                                           T *e_s, int lane) {
   if constexpr (MODE == MODE_F2) {
-    window_update_f2<NS, NCH, K1R>(mv, ids_s, m, k1, alpha, exact, sig_s, want, loss, cells,
-                                   rows_s, e_s, lane);
+    for (int r = lane; r < m + k1; r += 32) roff_s[r] = (uint32_t)ids_s[r] * (uint32_t)mv.ld;
+    __syncwarp();
+    window_update_f2<NS, NCH, K1R, K1R == 6>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss,
+                                             cells, rows_s, e_s, lane);
   } else {
     window_update<T, NCH, false, 0>(mv, ids_s, m, k1, alpha, exact, sig_s, want, loss, cells,
                                     rows_s, e_s, lane);
@@ -85,6 +90,7 @@ __device__ __forceinline__ void run_window(const ModelView<T> &mv, const int *id
 // ------------------------------------------------------- update_windows ----
 template <typename T> struct UpdateArgs {
   ModelView<T> mv;
+  int64_t vocab;
   const int32_t *in_off, *in_ids, *out_ids;
   int n_win, k1, mcap;
   const T *alpha, *sig;
@@ -106,6 +112,7 @@ __global__ void __launch_bounds__(256, MODE == MODE_F2 ? 2 : 1) update_windows_k
   T *rows_s = reinterpret_cast<T *>(base + L.rows);
   T *e_s = reinterpret_cast<T *>(base + L.e);
   int *ids_s = reinterpret_cast<int *>(base + L.ids);
+  uint32_t *roff_s = reinterpret_cast<uint32_t *>(base + L.roff);
   double loss = 0.0;
   long long cells = 0;
   for (int w = blockIdx.x * p.wpb + warp; w < p.n_win; w += gridDim.x * p.wpb) {
@@ -119,8 +126,8 @@ __global__ void __launch_bounds__(256, MODE == MODE_F2 ? 2 : 1) update_windows_k
       ids_s[r] = r < m ? p.in_ids[lo + r] : p.out_ids[(int64_t)w * p.k1 + (r - m)];
     __syncwarp();
     const bool want = p.loss_every > 0 && (w % p.loss_every) == 0;
-    run_window<T, MODE, NS, NCH, K1R>(p.mv, ids_s, m, p.k1, p.alpha[w], p.exact != 0, sig_s, want,
-                                      loss, cells, rows_s, e_s, lane);
+    run_window<T, MODE, NS, NCH, K1R>(p.mv, ids_s, roff_s, m, p.k1, p.alpha[w], p.exact != 0, sig_s,
+                                      want, loss, cells, rows_s, e_s, lane);
   }
   if (p.loss_every > 0) flush_loss<T>(loss, cells, p.loss_sum, p.loss_cells, true, lane);
 }
@@ -188,6 +195,7 @@ __global__ void __launch_bounds__(256, MODE == MODE_F2 ? 2 : 1) drive_kernel(Dri
   T *rows_s = reinterpret_cast<T *>(base + L.rows);
   T *e_s = reinterpret_cast<T *>(base + L.e);
   int *ids_s = reinterpret_cast<int *>(base + L.ids);
+  uint32_t *roff_s = reinterpret_cast<uint32_t *>(base + L.roff);
   int *kept_s = reinterpret_cast<int *>(base + L.kept);
   int *koff_s = reinterpret_cast<int *>(base + L.off);
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -380,8 +388,8 @@ __global__ void __launch_bounds__(256, MODE == MODE_F2 ? 2 : 1) drive_kernel(Dri
           if (lane == 0) p.trace_count[wid] = idx + 1;
         }
         if (p.update)
-          run_window<T, MODE, NS, NCH, K1R>(p.mv, ids_s, mc, k1, alpha_t, p.exact != 0, sig_s, want,
-                                            loss, cells, rows_s, e_s, lane);
+          run_window<T, MODE, NS, NCH, K1R>(p.mv, ids_s, roff_s, mc, k1, alpha_t, p.exact != 0, sig_s,
+                                            want, loss, cells, rows_s, e_s, lane);
         __syncwarp();
       }
       if (RNG == SGNS_RNG_SPLITMIX) rng = sb.state_after();
@@ -534,20 +542,21 @@ static int launch_drive_t(DriveArgs<T> a, int wpb_req, cudaStream_t st, int *res
   return (int)cudaGetLastError();
 }
 
-// float32 fast path: k1 <= 8 and d <= 512 (NS = float2 slots per lane)
+// float32 fast path: k1 <= 8, d <= 512 (NS = float2 slots per lane), V * ld < 2^32
 static int ns_for(int64_t ld_elems_f32) { return (int)((ld_elems_f32 / 2 + 31) / 32); }
+static bool offsets32_ok(int64_t vocab, int64_t ld) { return vocab * ld < (int64_t(1) << 32); }
 
 template <int NS, int RNG>
 static int drive_f2(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
   constexpr int NCH = (NS + 1) / 2;
-  if (a.k_neg + 1 <= 6) return launch_drive_t<float, MODE_F2, NS, NCH, 6, RNG>(a, wpb, st, res);
+  if (a.k_neg + 1 == 6) return launch_drive_t<float, MODE_F2, NS, NCH, 6, RNG>(a, wpb, st, res);
   return launch_drive_t<float, MODE_F2, NS, NCH, 8, RNG>(a, wpb, st, res);
 }
 
 template <int RNG>
 static int drive_f32(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
   const int ns = ns_for(a.mv.ld);
-  if (a.k_neg + 1 <= 8) {
+  if (a.k_neg + 1 <= 8 && offsets32_ok(a.vocab, a.mv.ld)) {
     switch (ns) {
       case 1: return drive_f2<1, RNG>(a, wpb, st, res);
       case 2: return drive_f2<2, RNG>(a, wpb, st, res);
@@ -584,13 +593,13 @@ static int drive_f64(DriveArgs<double> a, int wpb, cudaStream_t st, int *res) {
 template <int NS>
 static int update_f2(UpdateArgs<float> a, cudaStream_t st) {
   constexpr int NCH = (NS + 1) / 2;
-  if (a.k1 <= 6) return launch_update_t<float, MODE_F2, NS, NCH, 6>(a, st);
+  if (a.k1 == 6) return launch_update_t<float, MODE_F2, NS, NCH, 6>(a, st);
   return launch_update_t<float, MODE_F2, NS, NCH, 8>(a, st);
 }
 
 static int update_f32(UpdateArgs<float> a, cudaStream_t st) {
   const int ns = ns_for(a.mv.ld);
-  if (a.k1 <= 8) {
+  if (a.k1 <= 8 && offsets32_ok(a.vocab, a.mv.ld)) {
     switch (ns) {
       case 1: return update_f2<1>(a, st);
       case 2: return update_f2<2>(a, st);
@@ -735,7 +744,7 @@ int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, cons
                             static_cast<const float *>(d_m_in_src), static_cast<const float *>(d_m_out_src),
                             ld, (int)(ld / 4)};
     a.in_off = d_in_off; a.in_ids = d_in_ids; a.out_ids = d_out_ids;
-    a.n_win = n_windows; a.k1 = k1; a.mcap = max_inputs;
+    a.n_win = n_windows; a.k1 = k1; a.mcap = max_inputs; a.vocab = vocab;
     a.alpha = static_cast<const float *>(d_alpha);
     a.sig = static_cast<const float *>(d_sig_table);
     a.exact = sigmoid_mode == SGNS_SIGMOID_EXACT;
@@ -750,7 +759,7 @@ int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, cons
                              static_cast<const double *>(d_m_in_src),
                              static_cast<const double *>(d_m_out_src), ld, (int)(ld / 2)};
     a.in_off = d_in_off; a.in_ids = d_in_ids; a.out_ids = d_out_ids;
-    a.n_win = n_windows; a.k1 = k1; a.mcap = max_inputs;
+    a.n_win = n_windows; a.k1 = k1; a.mcap = max_inputs; a.vocab = vocab;
     a.alpha = static_cast<const double *>(d_alpha);
     a.sig = static_cast<const double *>(d_sig_table);
     a.exact = sigmoid_mode == SGNS_SIGMOID_EXACT;
