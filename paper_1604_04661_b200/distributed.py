@@ -201,7 +201,8 @@ def _device_run(vocab, encoded, config, alpha0_eff, total_x_epochs, sent_range, 
     corpus = DeviceCorpus(encoded, dm.m_in.device)
     sampler = DeviceSampler(vocab.counts, config.rng, config.table_length, None, dm.m_in.device)
     keep = vocab.keep_probs(config.subsample) if config.subsample > 0 else None
-    n_workers = default_workers(config, corpus, sent_range[1] - sent_range[0])
+    n_workers = default_workers(config, corpus, sent_range[1] - sent_range[0],
+                                int(encoded.offsets[sent_range[1]] - encoded.offsets[sent_range[0]]))
     return DeviceRun(dm, corpus, sampler, keep, config, alpha0_eff, total_x_epochs, n_workers,
                      sent_range=sent_range, stream_base=rank * n_workers)
 
