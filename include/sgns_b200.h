@@ -109,7 +109,18 @@ typedef struct sgns_drive_params {
   int32_t warps_per_block;       /* 0: default */
   int64_t token_base;            /* PHILOX: corpus position of d_ids[0] (streamed chunks) */
   int32_t epoch_base;            /* PHILOX: epoch index added to each worker's epoch */
+  /* SGNS_SCHEDULE_DYNAMIC (PHILOX, float32, k_neg + 1 <= 8, dim <= 512): workers claim
+   * sentence ordinals c in [*d_claim, claim_end) of the shard [shard_lo, shard_hi)
+   * (epoch = c / n, sentence = shard_lo + c % n); alpha from the sentence's words-read
+   * position words_base + epoch * shard_tokens + offset; d_workers only collects counters. */
+  int32_t schedule;
+  uint64_t *d_claim;
+  int64_t claim_end;
+  int64_t shard_lo, shard_hi;
+  int64_t words_base;
 } sgns_drive_params;
+
+enum { SGNS_SCHEDULE_STATIC = 0, SGNS_SCHEDULE_DYNAMIC = 1 };
 
 /* Fused resumable driver: every worker consumes up to word_budget words read. */
 int sgns_drive(const sgns_drive_params *p, void *stream);

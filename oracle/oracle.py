@@ -53,7 +53,7 @@ class Drive(C.Structure):
                 ("loss_every", C.c_int), ("workers", P), ("n_workers", C.c_int),
                 ("word_budget", I64), ("loss_by_epoch", P), ("cells_by_epoch", P),
                 ("update", C.c_int), ("trace_cap", I64), ("trace", P), ("trace_alpha", P),
-                ("trace_count", P)]
+                ("trace_count", P), ("position_mode", C.c_int)]
 
 
 assert _lib.or_sizeof_worker() == C.sizeof(Worker)
@@ -157,7 +157,7 @@ class OracleRun:
                  dynamic, seed, alpha0, floor_frac, total_x_epochs, epochs, loss_every,
                  n_workers, sent_range=None, stream_base=0, rng_mode="splitmix", slots=None,
                  alias=None, sig_table=None, refresh_words=10_000, trace_cap=0, update=True,
-                 use_exact=None):
+                 use_exact=None, position_mode=False):
         self.ids = np.ascontiguousarray(ids, dtype=np.int32)
         self.offsets = np.ascontiguousarray(offsets, dtype=np.int64)
         self.m_in, self.m_out = m_in, m_out
@@ -212,6 +212,7 @@ class OracleRun:
         d.trace = _p(self.trace) if trace_cap else None
         d.trace_alpha = _p(self.trace_alpha)
         d.trace_count = _p(self.trace_count)
+        d.position_mode = int(position_mode)
         self.d = d
 
     @property

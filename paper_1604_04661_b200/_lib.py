@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(HERE, LIB_NAME)
 SGNS_F32, SGNS_F64 = 0, 1
 SIGMOID_TABLE, SIGMOID_EXACT = 0, 1
 RNG_SPLITMIX, RNG_PHILOX = 0, 1
+SCHEDULE_STATIC, SCHEDULE_DYNAMIC = 0, 1
 
 P = C.c_void_p
 I32, I64, U64, F64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
@@ -41,6 +42,8 @@ class DriveParams(C.Structure):
         ("d_cells_by_epoch", P), ("update", I32), ("max_sentence", I32), ("trace_cap", I64),
         ("d_trace", P), ("d_trace_alpha", P), ("d_trace_count", P), ("d_error", P),
         ("warps_per_block", I32), ("token_base", I64), ("epoch_base", I32),
+        ("schedule", I32), ("d_claim", P), ("claim_end", I64), ("shard_lo", I64),
+        ("shard_hi", I64), ("words_base", I64),
     ]
 
 

@@ -1,0 +1,475 @@
+// sgns_fast.cuh -- production driver: Philox draws, dynamic sentence claiming and a
+// two-stage software pipeline across windows (float32, K + 1 <= 8, d <= 512).
+//
+// Differences from drive_kernel (the reference-stream driver), all invisible to the
+// update math:
+//  * workers claim sentences from one atomic counter per shard instead of owning a
+//    fixed range.  Philox draws are keyed by corpus position, so which worker trains a
+//    sentence does not change any draw; the step ends one sentence after the budget
+//    instead of at the slowest worker's range.
+//  * alpha of a sentence is computed from its exact words-read position
+//    (update_alpha, trainer.py:122-132) instead of a racy shared counter.
+//  * the loss proxy samples every loss_every-th sentence (uniform over progress).
+//  * pipeline: the negatives of window u+1 are drawn (Philox + alias loads in flight)
+//    before window u is computed, and u+1's output rows are loaded into registers as
+//    soon as u's dA loop no longer needs C -- i.e. during u's dC pass.  If u and u+1
+//    share an output row, u's dC is added to the prefetched copy, so every window still
+//    sees its worker's previous updates exactly (the reference's per-thread order).
+#pragma once
+
+#include "sgns_device.cuh"
+
+namespace sgns {
+
+__host__ __device__ inline int64_t round16_(int64_t b) { return (b + 15) & ~int64_t(15); }
+
+struct FastArgs {
+  ModelView<float> mv;
+  const int32_t *ids;
+  const int64_t *offsets;
+  const double *keep;
+  const uint32_t *alias_thr;
+  const int32_t *alias_idx;
+  uint32_t vocab;
+  uint32_t key0, key1;
+  int window, dynamic, k_neg, cap;
+  const float *sig;
+  double alpha0, floor_frac, total_x_epochs;
+  int64_t shard_lo, n_sent;
+  int epochs, loss_every;
+  unsigned long long *claim;  // next sentence ordinal
+  int64_t claim_end;          // exclusive
+  sgns_worker *workers;       // per-worker counters (chunks, trained, inputs)
+  int n_workers;
+  double *loss_by_epoch;      // [n_workers][epochs]
+  int64_t *cells_by_epoch;
+  int kept_cap;
+  int64_t trace_cap;          // total records (global), 0: off
+  int32_t *trace;
+  double *trace_alpha;
+  unsigned long long *trace_count;
+  int32_t *error;
+  int wpb;
+  int64_t token_base;
+  uint32_t epoch_base;
+  int64_t words_base;
+};
+
+struct FastSlab {
+  int64_t rows, e, ids, roff, kept, koff, bw, total;
+};
+__host__ __device__ inline FastSlab fast_slab(int64_t ld, int mcap, int k1r, int kept_cap) {
+  FastSlab s;
+  const int idsn = mcap + k1r;
+  s.rows = 0;
+  s.e = round16_(int64_t(mcap) * ld * 4);
+  s.ids = s.e + round16_(int64_t(mcap) * k1r * 4);
+  s.roff = s.ids + round16_(int64_t(2) * idsn * 4);
+  s.kept = s.roff + round16_(int64_t(2) * idsn * 4);
+  s.koff = s.kept + round16_(int64_t(kept_cap) * 4);
+  s.bw = s.koff + round16_(int64_t(kept_cap) * 4);
+  s.total = s.bw + round16_(int64_t(kept_cap) * 4);
+  return s;
+}
+
+// one window unit of a sentence: kept position pos, chunk index ch
+struct Unit {
+  int pos, ch, wlo, left, m, start, mc;
+};
+
+__device__ __forceinline__ bool unit_at(const int *bw_s, int nk, int cap, int pos, int ch, Unit &u) {
+  const int b = bw_s[pos];
+  const int wlo = max(pos - b, 0);
+  const int whi = min(pos + b + 1, nk);
+  const int m = whi - wlo - 1;
+  if (m <= 0 || ch * cap >= m) return false;
+  u.pos = pos;
+  u.ch = ch;
+  u.wlo = wlo;
+  u.left = pos - wlo;
+  u.m = m;
+  u.start = ch * cap;
+  u.mc = min(cap, m - u.start);
+  return true;
+}
+// next unit after (pos, ch) in the reference's order; false at the end of the sentence
+__device__ __forceinline__ bool next_unit(const int *bw_s, int nk, int cap, const Unit &cur, Unit &nx) {
+  if (unit_at(bw_s, nk, cap, cur.pos, cur.ch + 1, nx)) return true;
+  for (int pos = cur.pos + 1; pos < nk; ++pos)
+    if (unit_at(bw_s, nk, cap, pos, 0, nx)) return true;
+  return false;
+}
+__device__ __forceinline__ bool first_unit(const int *bw_s, int nk, int cap, Unit &nx) {
+  for (int pos = 0; pos < nk; ++pos)
+    if (unit_at(bw_s, nk, cap, pos, 0, nx)) return true;
+  return false;
+}
+
+// Candidate negative draws of one unit: lane j evaluates attempt (attempt0 + j).
+__device__ __forceinline__ int neg_candidate(const FastArgs &p, uint64_t tok, uint32_t ep, int ch,
+                                             uint32_t a) {
+  const uint4 o = philox_tok(tok, ep, kTagNeg | ((uint32_t)(ch & 0xFF) << 16) | ((a >> 1) & 0xFFFFu),
+                             p.key0, p.key1);
+  const uint32_t bw = (a & 1) ? o.z : o.x, coin = (a & 1) ? o.w : o.y;
+  const uint32_t bucket = (uint32_t)(((uint64_t)bw * (uint64_t)p.vocab) >> 32);
+  return coin < __ldg(p.alias_thr + bucket) ? (int)bucket : __ldg(p.alias_idx + bucket);
+}
+
+// Accept the first k_neg candidates != target (kernel_batched.py:57-66 semantics, with
+// the attempt sequence of the oracle's philox restatement); writes ids_s[mc+1 ...].
+__device__ __forceinline__ void select_negatives(const FastArgs &p, int cand, uint64_t tok, uint32_t ep,
+                                                 int ch, int target, int *ids_s, int mc, int lane) {
+  const unsigned lt = (1u << lane) - 1u;
+  int need = p.k_neg;
+  uint32_t attempt = 0;
+  int span = min(32, p.k_neg + 2);
+  while (true) {
+    const bool ok = lane < span && cand != target;
+    const unsigned mask = __ballot_sync(0xffffffffu, ok);
+    const int avail = __popc(mask);
+    const int take = min(avail, need);
+    const int rank = __popc(mask & lt);
+    if (ok && rank < take) ids_s[mc + 1 + (p.k_neg - need) + rank] = cand;
+    need -= take;
+    if (need == 0) break;
+    attempt += (uint32_t)span;  // every candidate of this span was consumed
+    span = min(32, need + 2);
+    cand = lane < span ? neg_candidate(p, tok, ep, ch, attempt + lane) : -1;
+  }
+}
+
+template <int NS, int NCH, int K1R, bool EXACT_K>
+__global__ void __launch_bounds__(256, 2) drive_fast_kernel(FastArgs p) {
+  constexpr int NV = 8;
+  extern __shared__ __align__(16) unsigned char smem[];
+  float *sig_s = reinterpret_cast<float *>(smem);
+  for (int i = threadIdx.x; i < kSigBins; i += blockDim.x) sig_s[i] = p.sig[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wid = blockIdx.x * p.wpb + warp;
+  if (wid >= p.n_workers) return;
+  const int k1 = EXACT_K ? K1R : p.k_neg + 1;
+  const int mcap = min(p.cap, 2 * p.window);
+  const FastSlab L = fast_slab(p.mv.ld, mcap, K1R, p.kept_cap);
+  unsigned char *base = smem + round16_(kSigBins * 4) + (int64_t)warp * L.total;
+  float *rows_s = reinterpret_cast<float *>(base + L.rows);
+  float *e_s = reinterpret_cast<float *>(base + L.e);
+  int *ids_b = reinterpret_cast<int *>(base + L.ids);
+  uint32_t *roff_b = reinterpret_cast<uint32_t *>(base + L.roff);
+  int *kept_s = reinterpret_cast<int *>(base + L.kept);
+  int *koff_s = reinterpret_cast<int *>(base + L.koff);
+  int *bw_s = reinterpret_cast<int *>(base + L.bw);
+  const int idsn = mcap + K1R;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t ld = p.mv.ld;
+  const int nvec = p.mv.nvec, nslot = 2 * nvec;
+  auto slot_ok = [&](int j) { return j < NS - 1 || lane + 32 * j < nslot; };
+  auto chunk_ok = [&](int j) { return j < NCH - 1 || lane + 32 * j < nvec; };
+  auto kk_ok = [&](int k) { return EXACT_K || k < k1; };
+  const int my_k = reduced_index<NV>(lane);
+  const bool leader = (lane & ((32 / NV) - 1)) == 0;
+  const int64_t off0 = p.offsets[p.shard_lo];
+  const int64_t shard_tokens = p.offsets[p.shard_lo + p.n_sent] - off0;
+  const int rec_len = 4 + p.cap + k1;
+
+  long long chunks = 0, trained = 0, inputs = 0;
+  double loss = 0.0;
+  long long cells = 0;
+  int loss_epoch = -1;
+
+  for (;;) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(p.claim, 1ULL);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if ((int64_t)c >= p.claim_end) break;
+    const int epoch = (int)((int64_t)c / p.n_sent);
+    const int64_t s = p.shard_lo + (int64_t)c % p.n_sent;
+    const int64_t lo_t = p.offsets[s], hi_t = p.offsets[s + 1];
+    const int n = (int)(hi_t - lo_t);
+    if (n > p.kept_cap) {
+      if (lane == 0 && p.error) atomicExch(p.error, 2);
+      continue;
+    }
+    const uint32_t ep = p.epoch_base + (uint32_t)epoch;
+    // alpha from the sentence's words-read position (update_alpha, trainer.py:122-132)
+    const double pos_words = (double)(p.words_base + (int64_t)epoch * shard_tokens + (lo_t - off0));
+    double frac = 1.0 - pos_words / (p.total_x_epochs + 1.0);
+    if (frac < p.floor_frac) frac = p.floor_frac;
+    const float alpha = (float)(p.alpha0 * frac);
+    const bool want = p.loss_every > 0 && ((int64_t)c % p.loss_every) == 0;
+    if (want && epoch != loss_epoch) {
+      if (loss_epoch >= 0) {
+        double l2 = loss;
+        long long c2 = cells;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          l2 += __shfl_xor_sync(0xffffffffu, l2, o);
+          c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+        }
+        if (lane == 0) {
+          p.loss_by_epoch[(int64_t)wid * p.epochs + loss_epoch] += l2;
+          p.cells_by_epoch[(int64_t)wid * p.epochs + loss_epoch] += c2;
+        }
+        loss = 0.0;
+        cells = 0;
+      }
+      loss_epoch = epoch;
+    }
+    // subsample: one Philox uniform per token, survivors compacted in order
+    int nk = 0;
+    for (int b0 = 0; b0 < n; b0 += 32) {
+      const int i = b0 + lane;
+      const bool valid = i < n;
+      const int w = valid ? p.ids[lo_t + i] : 0;
+      bool keep = valid;
+      if (p.keep != nullptr && valid) {
+        const uint4 o = philox_tok((uint64_t)(p.token_base + lo_t + i), ep, kTagSub, p.key0, p.key1);
+        keep = u53((uint64_t)o.x | ((uint64_t)o.y << 32)) < p.keep[w];
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int q = nk + __popc(mask & lt_mask);
+        kept_s[q] = w;
+        koff_s[q] = i;
+      }
+      nk += __popc(mask);
+    }
+    __syncwarp();
+    // dynamic half-widths of every kept position, lane-parallel
+    for (int q = lane; q < nk; q += 32) {
+      int b = p.window;
+      if (p.dynamic) {
+        const uint4 o = philox_tok((uint64_t)(p.token_base + lo_t + koff_s[q]), ep, kTagWin, p.key0, p.key1);
+        b = 1 + (int)(((uint64_t)o.x * (uint64_t)p.window) >> 32);
+      }
+      bw_s[q] = b;
+    }
+    __syncwarp();
+    trained += nk;
+
+    Unit u;
+    if (!first_unit(bw_s, nk, p.cap, u)) continue;
+    // window u's inputs + target + negatives (synchronous for the first unit)
+    int cur = 0;
+    {
+      int *ids_s = ids_b;
+      for (int r = lane; r < u.mc; r += 32) {
+        const int q = u.start + r;
+        ids_s[r] = q < u.left ? kept_s[u.wlo + q] : kept_s[u.pos + 1 + (q - u.left)];
+      }
+      const int target = kept_s[u.pos];
+      if (lane == 0) ids_s[u.mc] = target;
+      const uint64_t tok = (uint64_t)(p.token_base + lo_t + koff_s[u.pos]);
+      const int cand = lane < min(32, p.k_neg + 2) ? neg_candidate(p, tok, ep, u.ch, lane) : -1;
+      select_negatives(p, cand, tok, ep, u.ch, target, ids_s, u.mc, lane);
+      __syncwarp();
+      for (int r = lane; r < u.mc + k1; r += 32) roff_b[r] = (uint32_t)ids_s[r] * (uint32_t)ld;
+      __syncwarp();
+    }
+    // C rows of u -> registers
+    float2 c_reg[K1R][NS];
+    {
+      const uint32_t *off_s = roff_b;
+#pragma unroll
+      for (int k = 0; k < K1R; ++k) {
+        const float *src = p.mv.out_src + off_s[u.mc + (kk_ok(k) ? k : 0)];
+#pragma unroll
+        for (int j = 0; j < NS; ++j)
+          c_reg[k][j] = (kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 2 * (lane + 32 * j)) : f2zero();
+      }
+    }
+    bool have = true;
+    while (have) {
+      int *ids_s = ids_b + cur * idsn;
+      const uint32_t *off_s = roff_b + cur * idsn;
+      int *ids_n = ids_b + (cur ^ 1) * idsn;
+      uint32_t *off_n = roff_b + (cur ^ 1) * idsn;
+      const int m = u.mc;
+      // A rows of u -> smem
+      for (int r = 0; r < m; ++r) {
+        const float *src = p.mv.in_src + off_s[r];
+        float *dst = rows_s + (int64_t)r * ld;
+#pragma unroll
+        for (int j = 0; j < NCH; ++j)
+          if (chunk_ok(j)) cp_async16(dst + (lane + 32 * j) * 4, src + (lane + 32 * j) * 4);
+      }
+      // next unit + its negative candidates (alias loads in flight during u's math)
+      Unit nx;
+      have = next_unit(bw_s, nk, p.cap, u, nx);
+      int cand_n = -1;
+      uint64_t tok_n = 0;
+      if (have) {
+        tok_n = (uint64_t)(p.token_base + lo_t + koff_s[nx.pos]);
+        if (lane < min(32, p.k_neg + 2)) cand_n = neg_candidate(p, tok_n, ep, nx.ch, lane);
+      }
+      chunks += 1;
+      inputs += m;
+      if (p.trace_cap > 0) {
+        unsigned long long idx = 0;
+        if (lane == 0) idx = atomicAdd(p.trace_count, 1ULL);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if ((int64_t)idx < p.trace_cap) {
+          int32_t *rec = p.trace + (int64_t)idx * rec_len;
+          for (int r = lane; r < rec_len; r += 32) {
+            int v;
+            if (r == 0) v = ids_s[m];
+            else if (r == 1) v = m;
+            else if (r == 2) v = (int)s;
+            else if (r == 3) v = epoch;
+            else if (r < 4 + p.cap) v = (r - 4) < m ? ids_s[r - 4] : -1;
+            else v = ids_s[m + (r - 4 - p.cap)];
+            rec[r] = v;
+          }
+          if (lane == 0) p.trace_alpha[idx] = (double)alpha;
+        }
+      }
+      cp_async_wait_all();
+      __syncwarp();
+
+      // scores, errors, dA
+      const float2 alpha2 = make_float2(alpha, alpha);
+      for (int i = 0; i < m; ++i) {
+        float2 a[NS];
+#pragma unroll
+        for (int j = 0; j < NS; ++j)
+          a[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + 2 * (lane + 32 * j))
+                            : f2zero();
+        float pp[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          if (k < K1R) {
+            float2 acc = __fmul2_rn(a[0], c_reg[k][0]);
+#pragma unroll
+            for (int j = 1; j < NS; ++j) acc = __ffma2_rn(a[j], c_reg[k][j], acc);
+            pp[k] = acc.x + acc.y;
+          } else {
+            pp[k] = 0.f;
+          }
+        }
+        const float sc = transpose_reduce<NV>(pp, lane);
+        float er = 0.f, es = 0.f;
+        if (my_k < k1) {
+          cell_error<float>(sc, my_k, alpha, false, sig_s, er, es);
+          if (leader) {
+            e_s[i * K1R + my_k] = es;
+            if (want) {
+              loss += softplus(my_k == 0 ? -(double)sc : (double)sc);
+              cells += 1;
+            }
+          }
+        }
+        float2 d[NS];
+#pragma unroll
+        for (int k = 0; k < K1R; ++k) {
+          const float ek = __shfl_sync(0xffffffffu, er, group_leader<NV>(k));
+          const float2 ek2 = make_float2(ek, ek);
+#pragma unroll
+          for (int j = 0; j < NS; ++j)
+            d[j] = k == 0 ? __fmul2_rn(ek2, c_reg[0][j]) : __ffma2_rn(ek2, c_reg[k][j], d[j]);
+        }
+        float *dst = p.mv.in_dst + off_s[i];
+#pragma unroll
+        for (int j = 0; j < NS; ++j)
+          if (slot_ok(j))
+            atomicAdd(reinterpret_cast<float2 *>(dst + 2 * (lane + 32 * j)), __fmul2_rn(d[j], alpha2));
+      }
+      // C registers are free: finish u+1's negatives and start loading its output rows
+      // bit (8 k + k') of lo_bits (k < 4) / hi_bits (k >= 4): out(u)[k] == out(u+1)[k']
+      unsigned lo_bits = 0, hi_bits = 0;
+      if (have) {
+        for (int r = lane; r < nx.mc; r += 32) {
+          const int q = nx.start + r;
+          ids_n[r] = q < nx.left ? kept_s[nx.wlo + q] : kept_s[nx.pos + 1 + (q - nx.left)];
+        }
+        const int target = kept_s[nx.pos];
+        if (lane == 0) ids_n[nx.mc] = target;
+        select_negatives(p, cand_n, tok_n, ep, nx.ch, target, ids_n, nx.mc, lane);
+        __syncwarp();
+        for (int r = lane; r < nx.mc + k1; r += 32) off_n[r] = (uint32_t)ids_n[r] * (uint32_t)ld;
+        const int kq = lane & 7, ka = lane >> 3, kb = 4 + (lane >> 3);
+        const bool h1 = ka < k1 && kq < k1 && ids_s[m + ka] == ids_n[nx.mc + kq];
+        const bool h2 = kb < k1 && kq < k1 && ids_s[m + kb] == ids_n[nx.mc + kq];
+        lo_bits = __ballot_sync(0xffffffffu, h1);
+        hi_bits = __ballot_sync(0xffffffffu, h2);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < K1R; ++k) {
+          const float *src = p.mv.out_src + off_n[nx.mc + (kk_ok(k) ? k : 0)];
+#pragma unroll
+          for (int j = 0; j < NS; ++j)
+            c_reg[k][j] = (kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 2 * (lane + 32 * j)) : f2zero();
+        }
+      }
+      __syncwarp();
+      // dC_k = sum_i (alpha err_ik) A_i, column-outer; patch u+1's prefetched copies
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+        if (!slot_ok(j)) continue;
+        const int col = 2 * (lane + 32 * j);
+        float2 acc[K1R];
+#pragma unroll
+        for (int k = 0; k < K1R; ++k) acc[k] = f2zero();
+        int i = 0;
+        for (; i + 1 < m; i += 2) {
+          const float2 a0 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col);
+          const float2 a1 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)(i + 1) * ld + col);
+#pragma unroll
+          for (int k = 0; k < K1R; ++k)
+            if (kk_ok(k)) {
+              const float e0 = e_s[i * K1R + k], e1 = e_s[(i + 1) * K1R + k];
+              acc[k] = __ffma2_rn(make_float2(e0, e0), a0, acc[k]);
+              acc[k] = __ffma2_rn(make_float2(e1, e1), a1, acc[k]);
+            }
+        }
+        if (i < m) {
+          const float2 a0 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col);
+#pragma unroll
+          for (int k = 0; k < K1R; ++k)
+            if (kk_ok(k)) {
+              const float e0 = e_s[i * K1R + k];
+              acc[k] = __ffma2_rn(make_float2(e0, e0), a0, acc[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K1R; ++k)
+          if (kk_ok(k)) atomicAdd(reinterpret_cast<float2 *>(p.mv.out_dst + off_s[m + k] + col), acc[k]);
+        if (lo_bits | hi_bits) {
+#pragma unroll
+          for (int k = 0; k < K1R; ++k) {
+            const unsigned row = k < 4 ? (lo_bits >> (8 * k)) & 0xFFu : (hi_bits >> (8 * (k - 4))) & 0xFFu;
+            if (row) {
+#pragma unroll
+              for (int kq = 0; kq < K1R; ++kq)
+                if (row & (1u << kq)) c_reg[kq][j] = __fadd2_rn(c_reg[kq][j], acc[k]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (have) {
+        u = nx;
+        cur ^= 1;
+      }
+    }
+  }
+  // flush this worker's counters
+  if (loss_epoch >= 0) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      loss += __shfl_xor_sync(0xffffffffu, loss, o);
+      cells += __shfl_xor_sync(0xffffffffu, cells, o);
+    }
+    if (lane == 0) {
+      p.loss_by_epoch[(int64_t)wid * p.epochs + loss_epoch] += loss;
+      p.cells_by_epoch[(int64_t)wid * p.epochs + loss_epoch] += cells;
+    }
+  }
+  if (lane == 0) {
+    sgns_worker &o = p.workers[wid];
+    o.kernel_counter += chunks;
+    o.words_trained += trained;
+    o.inputs += inputs;
+  }
+}
+
+}  // namespace sgns

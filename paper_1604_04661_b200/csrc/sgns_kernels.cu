@@ -16,6 +16,7 @@
 
 #include "../../include/sgns_b200.h"
 #include "sgns_device.cuh"
+#include "sgns_fast.cuh"
 
 namespace sgns {
 
@@ -676,7 +677,100 @@ static void fill_drive_args(DriveArgs<T> &a, const sgns_drive_params *p) {
   a.epoch_base = (uint32_t)p->epoch_base;
 }
 
+// ------------------------------------------------------------ fast path ----
+template <int NS, int K1R, bool EXACT>
+static int launch_fast_t(FastArgs a, int wpb_req, cudaStream_t st, int *resident) {
+  constexpr int NCH = (NS + 1) / 2;
+  auto kern = drive_fast_kernel<NS, NCH, K1R, EXACT>;
+  const FastSlab L = fast_slab(a.mv.ld, std::min(a.cap, 2 * a.window), K1R, a.kept_cap);
+  int wpb = 0, bps = 0;
+  int rc = choose_wpb(kern, table_bytes(4), L.total, &wpb, &bps);
+  if (rc) return rc;
+  if (resident) {
+    *resident = wpb * bps * num_sms();
+    return 0;
+  }
+  if (wpb_req > 0) wpb = wpb_req;
+  a.wpb = wpb;
+  const int64_t bytes = table_bytes(4) + (int64_t)wpb * L.total;
+  if ((rc = prepare(kern, bytes))) return rc;
+  const int grid = (a.n_workers + wpb - 1) / wpb;
+  kern<<<grid, wpb * 32, bytes, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+template <int NS>
+static int fast_ns(FastArgs a, int wpb, cudaStream_t st, int *res) {
+  if (a.k_neg + 1 == 6) return launch_fast_t<NS, 6, true>(a, wpb, st, res);
+  return launch_fast_t<NS, 8, false>(a, wpb, st, res);
+}
+
+static bool fast_eligible(const sgns_drive_params *p) {
+  const int64_t ld = p->ld;
+  return p->dtype == SGNS_F32 && p->rng_mode == SGNS_RNG_PHILOX && p->k_neg + 1 <= 8 &&
+         ns_for(ld) >= 1 && ns_for(ld) <= 8 && offsets32_ok(p->vocab, ld) &&
+         p->sigmoid_mode == SGNS_SIGMOID_TABLE;
+}
+
+static int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
+  FastArgs a;
+  std::memset(&a, 0, sizeof(a));
+  float *mi = static_cast<float *>(p->d_m_in), *mo = static_cast<float *>(p->d_m_out);
+  a.mv = ModelView<float>{mi, mo, mi, mo, p->ld, (int)(p->ld * 4 / 16)};
+  a.ids = p->d_ids;
+  a.offsets = p->d_offsets;
+  a.keep = p->d_keep_probs;
+  a.alias_thr = p->d_alias_thr;
+  a.alias_idx = p->d_alias_idx;
+  a.vocab = (uint32_t)p->vocab;
+  a.key0 = (uint32_t)p->seed;
+  a.key1 = (uint32_t)(p->seed >> 32);
+  a.window = p->window;
+  a.dynamic = p->dynamic;
+  a.k_neg = p->k_neg;
+  a.cap = p->batch_cap;
+  a.sig = static_cast<const float *>(p->d_sig_table);
+  a.alpha0 = p->alpha0;
+  a.floor_frac = p->floor_frac;
+  a.total_x_epochs = p->total_x_epochs;
+  a.shard_lo = p->shard_lo;
+  a.n_sent = p->shard_hi - p->shard_lo;
+  a.epochs = p->epochs;
+  a.loss_every = p->loss_every;
+  a.claim = reinterpret_cast<unsigned long long *>(p->d_claim);
+  a.claim_end = p->claim_end;
+  a.workers = p->d_workers;
+  a.n_workers = p->n_workers;
+  a.loss_by_epoch = p->d_loss_by_epoch;
+  a.cells_by_epoch = p->d_cells_by_epoch;
+  a.kept_cap = ((std::max(p->max_sentence, 1) + 31) / 32) * 32;
+  a.trace_cap = p->trace_cap;
+  a.trace = p->d_trace;
+  a.trace_alpha = p->d_trace_alpha;
+  a.trace_count = reinterpret_cast<unsigned long long *>(p->d_trace_count);
+  a.error = p->d_error;
+  a.token_base = p->token_base;
+  a.epoch_base = (uint32_t)p->epoch_base;
+  a.words_base = p->words_base;
+  const int wpb = p->warps_per_block;
+  switch (ns_for(p->ld)) {
+    case 1: return fast_ns<1>(a, wpb, st, resident);
+    case 2: return fast_ns<2>(a, wpb, st, resident);
+    case 3: return fast_ns<3>(a, wpb, st, resident);
+    case 4: return fast_ns<4>(a, wpb, st, resident);
+    case 5: return fast_ns<5>(a, wpb, st, resident);
+    case 6: return fast_ns<6>(a, wpb, st, resident);
+    case 7: return fast_ns<7>(a, wpb, st, resident);
+    case 8: return fast_ns<8>(a, wpb, st, resident);
+  }
+  return SGNS_E_SHAPE;
+}
+
 static int drive_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
+  if (p->schedule == SGNS_SCHEDULE_DYNAMIC) {
+    if (!fast_eligible(p)) return SGNS_E_ARG;
+    return fast_dispatch(p, st, resident);
+  }
   const int wpb = p->warps_per_block;
   if (p->dtype == SGNS_F32) {
     DriveArgs<float> a;
@@ -784,6 +878,8 @@ int sgns_drive(const sgns_drive_params *p, void *stream) {
   if (p->rng_mode == SGNS_RNG_PHILOX && (!p->d_alias_thr || !p->d_alias_idx)) return SGNS_E_ARG;
   if (p->rng_mode != SGNS_RNG_SPLITMIX && p->rng_mode != SGNS_RNG_PHILOX) return SGNS_E_ARG;
   if (p->trace_cap > 0 && (!p->d_trace || !p->d_trace_alpha || !p->d_trace_count)) return SGNS_E_ARG;
+  if (p->schedule == SGNS_SCHEDULE_DYNAMIC &&
+      (!p->d_claim || p->shard_hi <= p->shard_lo || p->shard_lo < 0)) return SGNS_E_ARG;
   if (p->dtype != SGNS_F32 && p->dtype != SGNS_F64) return SGNS_E_ARG;
   return drive_dispatch(p, static_cast<cudaStream_t>(stream), nullptr);
 }
@@ -835,6 +931,8 @@ int sgns_resident_workers(int32_t dtype, int32_t dim, int32_t window, int32_t k_
   p.batch_cap = batch_cap;
   p.max_sentence = max_sentence;
   p.rng_mode = SGNS_RNG_PHILOX;
+  p.sigmoid_mode = dtype == SGNS_F64 ? SGNS_SIGMOID_EXACT : SGNS_SIGMOID_TABLE;
+  p.schedule = fast_eligible(&p) ? SGNS_SCHEDULE_DYNAMIC : SGNS_SCHEDULE_STATIC;
   int resident = 0;
   const int rc = drive_dispatch(&p, nullptr, &resident);
   if (rc) return rc;

@@ -197,6 +197,9 @@ class DistributedRunError(RuntimeError):
 def _device_run(vocab, encoded, config, alpha0_eff, total_x_epochs, sent_range, rank, device):
     """Default engine: this rank's shard on its GPU (DeviceRun over W workers)."""
     from .model import init_device_model
+    import torch
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
     dm = init_device_model(vocab.size, config.dim, config.seed, config.dtype, device)
     corpus = DeviceCorpus(encoded, dm.m_in.device)
     sampler = DeviceSampler(vocab.counts, config.rng, config.table_length, None, dm.m_in.device)

@@ -72,6 +72,7 @@ class TrainingConfig:
     rng: str = "philox"                   # "philox" (production) | "splitmix" (reference stream)
     workers: int | None = None            # None: splitmix -> threads; philox -> resident warps
     alpha_refresh_words: int | None = None  # None: splitmix -> 10,000; philox -> every sentence
+    schedule: str = "auto"                # "auto" | "static" (fixed ranges) | "dynamic" (claims)
 
     def validate(self) -> None:
         if self.dim < 1:
@@ -106,6 +107,20 @@ class TrainingConfig:
             raise ConfigError("workers must be >= 1")
         if self.alpha_refresh_words is not None and self.alpha_refresh_words < 1:
             raise ConfigError("alpha_refresh_words must be >= 1")
+        if self.schedule not in ("auto", "static", "dynamic"):
+            raise ConfigError(f"unknown schedule {self.schedule!r}")
+        if self.schedule == "dynamic" and not self.dynamic_eligible(0):
+            raise ConfigError("schedule='dynamic' needs rng='philox', float32, negatives <= 7, dim <= 512")
+
+    def dynamic_eligible(self, vocab_size: int) -> bool:
+        ld = -(-self.dim // 4) * 4
+        return (self.rng == "philox" and not self.float64 and self.negatives + 1 <= 8
+                and -(-(ld // 2) // 32) <= 8 and vocab_size * ld < 2**32)
+
+    def use_dynamic(self, vocab_size: int) -> bool:
+        if self.schedule == "static":
+            return False
+        return self.dynamic_eligible(vocab_size)
 
     @property
     def dtype(self):
@@ -275,14 +290,69 @@ class DeviceRun:
             p.d_trace, p.d_trace_alpha = self.trace.data_ptr(), self.trace_alpha.data_ptr()
             p.d_trace_count = self.trace_count.data_ptr()
         p.d_error = self.error.data_ptr()
+        self.dynamic = config.use_dynamic(model.vocab_size)
+        if self.dynamic:
+            # sentence ordinals c in [0, epochs * n) of the shard, claimed by the workers
+            self.shard_lo, self.shard_hi = lo, hi
+            self.n_sent = hi - lo
+            offs = corpus.host_offsets
+            self._offs = offs
+            self.shard_tokens = int(offs[hi] - offs[lo])
+            self.total_claims = config.epochs * self.n_sent
+            self.claim_pos = 0
+            self.claim = torch.zeros(1, dtype=torch.int64, device=dev)
+            p.schedule = _lib.SCHEDULE_DYNAMIC
+            p.d_claim = self.claim.data_ptr()
+            p.shard_lo, p.shard_hi = lo, hi
+            self._dyn_read = 0
+            if trace_cap:
+                self.trace = torch.full((trace_cap, self.rec_len), -1, dtype=torch.int32, device=dev)
+                self.trace_alpha = torch.zeros(trace_cap, dtype=torch.float64, device=dev)
+                self.trace_count = torch.zeros(1, dtype=torch.int64, device=dev)
+                p.d_trace, p.d_trace_alpha = self.trace.data_ptr(), self.trace_alpha.data_ptr()
+                p.d_trace_count = self.trace_count.data_ptr()
         self.params = p
         self._host_state = None
 
+    # -- dynamic schedule helpers -------------------------------------------
+    def words_at(self, c: int) -> int:
+        """Words read by this shard before sentence ordinal c (epoch-major)."""
+        if self.n_sent == 0:
+            return 0
+        e, r = divmod(int(c), self.n_sent)
+        return e * self.shard_tokens + int(self._offs[self.shard_lo + r] - self._offs[self.shard_lo])
+
+    def _claim_end(self, budget_total: int) -> int:
+        start = self.claim_pos
+        target = self.words_at(start) + budget_total
+        lo, hi = start + 1, self.total_claims
+        if lo > hi:
+            return hi
+        if self.words_at(hi) < target:
+            return hi
+        while lo < hi:  # smallest c with words_at(c) >= target
+            mid = (lo + hi) // 2
+            if self.words_at(mid) >= target:
+                hi = mid
+            else:
+                lo = mid + 1
+        return lo
+
     # -- launches ---------------------------------------------------------
     def launch(self, word_budget: int, stream=None) -> None:
-        """Stream-ordered: every worker consumes up to word_budget words read."""
+        """Stream-ordered: every worker consumes up to word_budget words read
+        (dynamic schedule: the workers together consume n_workers * word_budget)."""
         self.params.word_budget = int(word_budget)
         st = current_stream_ptr(self.device) if stream is None else stream
+        if self.dynamic:
+            if self.claim_pos >= self.total_claims:
+                return
+            total = min(int(word_budget) * self.n_workers, 2**62)
+            end = self._claim_end(total)
+            self.claim.fill_(self.claim_pos)
+            self.params.claim_end = end
+            self._dyn_read += self.words_at(end) - self.words_at(self.claim_pos)
+            self.claim_pos = end
         _lib.check(_lib.lib().sgns_drive(self.params, st), "sgns_drive")
         self._host_state = None
 
@@ -296,10 +366,14 @@ class DeviceRun:
 
     @property
     def done(self) -> bool:
+        if self.dynamic:
+            return self.claim_pos >= self.total_claims
         return bool(self.state()["done"].all())
 
     @property
     def words_read(self) -> int:
+        if self.dynamic:
+            return self._dyn_read
         return int(self.state()["words_read"].sum())
 
     @property
@@ -314,7 +388,7 @@ class DeviceRun:
 
     def run_to_completion(self) -> None:
         while not self.done:
-            self.launch(_INF_BUDGET)
+            self.launch(_INF_BUDGET // max(self.n_workers, 1))
 
     def loss_by_epoch(self) -> list[float]:
         ls = self.loss.sum(dim=0).cpu().numpy()
@@ -322,7 +396,14 @@ class DeviceRun:
         return [float(a / b) if b else 0.0 for a, b in zip(ls, cs)]
 
     def shared_words_read(self) -> int:
+        if self.dynamic:
+            return self.words_at(self.claim_pos)
         return int(self.shared[0].item())
+
+    def trace_records(self):
+        """Dynamic schedule: every traced window (processing order across workers)."""
+        n = min(int(self.trace_count[0].item()), self.trace_cap)
+        return self.trace[:n].cpu().numpy(), self.trace_alpha[:n].cpu().numpy()
 
     def worker_trace(self, w: int):
         n = min(int(self.trace_count[w].item()), self.trace_cap)
@@ -398,21 +479,22 @@ def train(corpus_path: str, config: TrainingConfig, progress: bool = False):
 
 class StreamingTrainer:
     """Out-of-core training: sentence chunks stream from (pinned) host memory
-    through preallocated HBM buffers while the model, sampler and the shared
-    alpha schedule stay resident.  Each `train_chunk` call is one host->device
-    copy, one driver launch over the chunk (its workers re-split the chunk by
-    tokens), and one tiny device->host read of the chunk's counters.  With
-    rng="philox" the draws are keyed by the global corpus position
-    (`token_base`), so streaming does not change which windows are drawn."""
+    through preallocated HBM buffers while the model, sampler and alpha
+    schedule stay resident.  Each `train_chunk` is one host->device copy, one
+    driver launch over the chunk (dynamic schedule: workers claim its
+    sentences), and one small device->host read of the chunk's counters.
+    Draws are keyed by the global corpus position (`token_base`) and alpha by
+    the global words-read position, so chunking does not change the training."""
 
     def __init__(self, model: DeviceModel, counts: np.ndarray, config: TrainingConfig,
                  total_x_epochs: float, max_chunk_tokens: int, max_chunk_sentences: int,
                  max_sentence: int, n_workers: int | None = None, alpha0_eff: float | None = None,
-                 total_tokens: int | None = None, keep_probs: np.ndarray | None = None):
+                 keep_probs: np.ndarray | None = None):
         torch = _torch()
         config.validate()
-        if config.rng != "philox":
-            raise ConfigError("streaming training needs rng='philox' (position-keyed draws)")
+        if not config.use_dynamic(model.vocab_size):
+            raise ConfigError("streaming training needs the dynamic schedule "
+                              "(rng='philox', float32, negatives <= 7, dim <= 512)")
         self.torch = torch
         self.model, self.config = model, config
         dev = model.m_in.device
@@ -430,16 +512,14 @@ class StreamingTrainer:
         self.n_workers = n_workers
         self.alpha0_eff = config.alpha0 if alpha0_eff is None else alpha0_eff
         self.total_x_epochs = total_x_epochs
-        self.alpha = self.alpha0_eff
-        self.workers_host = torch.zeros((n_workers * WORKER_DTYPE.itemsize,), dtype=torch.uint8).pin_memory()
-        self.workers = torch.zeros_like(self.workers_host, device=dev)
-        self.shared = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.workers = torch.zeros((n_workers * WORKER_DTYPE.itemsize,), dtype=torch.uint8, device=dev)
+        self.claim = torch.zeros(1, dtype=torch.int64, device=dev)
         self.loss = torch.zeros((n_workers, 1), dtype=torch.float64, device=dev)
         self.cells = torch.zeros((n_workers, 1), dtype=torch.int64, device=dev)
+        self.shared = torch.zeros(2, dtype=torch.int64, device=dev)
         self.stats_dev = torch.zeros(6, dtype=torch.float64, device=dev)
         self.stats_host = torch.zeros(6, dtype=torch.float64).pin_memory()
         self.sig = device_sigmoid_table(model.np_dtype, dev)
-        self.max_sentence = max_sentence
         p = _lib.DriveParams()
         p.dtype = model.cdtype
         p.d_m_in, p.d_m_out = model.m_in.data_ptr(), model.m_out.data_ptr()
@@ -451,7 +531,7 @@ class StreamingTrainer:
         p.seed = config.seed & (2**64 - 1)
         p.window, p.dynamic, p.k_neg = config.window, int(config.dynamic_window), config.negatives
         p.batch_cap = config.batch_cap
-        p.sigmoid_mode = _lib.SIGMOID_EXACT if config.float64 else _lib.SIGMOID_TABLE
+        p.sigmoid_mode = _lib.SIGMOID_TABLE
         p.d_sig_table = self.sig.data_ptr()
         p.alpha0, p.floor_frac = self.alpha0_eff, config.alpha_floor_fraction
         p.total_x_epochs = total_x_epochs
@@ -463,40 +543,45 @@ class StreamingTrainer:
         p.update = 1
         p.max_sentence = max(max_sentence, 1)
         p.word_budget = _INF_BUDGET
+        p.schedule = _lib.SCHEDULE_DYNAMIC
+        p.d_claim = self.claim.data_ptr()
+        p.shard_lo = 0
         self.params = p
         self.h2d_bytes = 0
         self.d2h_bytes = 0
 
-    def train_chunk(self, ids_host, offsets_host: np.ndarray, token_base: int, epoch: int = 0):
-        """Train one chunk; ids_host: pinned torch int32 tensor of the chunk's tokens,
-        offsets_host: int64 sentence offsets of the chunk starting at 0.  Returns the
-        chunk's (words_trained, words_read, loss_sum, loss_cells, inputs, chunks)."""
+    def train_chunk(self, ids_host, offsets_host: np.ndarray, token_base: int, epoch: int = 0,
+                    words_base: int | None = None):
+        """Train one chunk.  ids_host: pinned torch int32 tensor of its tokens;
+        offsets_host: its int64 sentence offsets starting at 0; token_base: corpus
+        position of its first token; words_base: words read before it (default
+        token_base).  Returns (words_trained, words_read, loss_sum, loss_cells,
+        inputs, chunks) of the chunk."""
         torch = self.torch
         n_tok = int(offsets_host[-1])
         n_sent = len(offsets_host) - 1
+        if n_sent < 1:
+            return 0, 0, 0.0, 0, 0, 0
         if n_tok > self.ids.numel() or n_sent + 1 > self.offsets.numel():
             raise ValueError("chunk larger than the streaming buffers")
         self.ids[:n_tok].copy_(ids_host[:n_tok], non_blocking=True)
         off_t = torch.from_numpy(np.ascontiguousarray(offsets_host, dtype=np.int64))
-        self.offsets[:n_sent + 1].copy_(off_t, non_blocking=False)
-        ranges = split_by_tokens(offsets_host, 0, n_sent, self.n_workers)
-        w = self.workers_host.numpy().view(WORKER_DTYPE)
-        w[:] = 0
-        w["lo"] = [a for a, _ in ranges]
-        w["next_sent"] = w["lo"]
-        w["hi"] = [b for _, b in ranges]
-        w["alpha"] = self.alpha
-        self.workers.copy_(self.workers_host, non_blocking=True)
+        self.offsets[:n_sent + 1].copy_(off_t)
+        self.workers.zero_()
         self.loss.zero_()
         self.cells.zero_()
-        self.params.token_base = int(token_base)
-        self.params.epoch_base = int(epoch)
-        st = current_stream_ptr(self.device)
-        _lib.check(_lib.lib().sgns_drive(self.params, st), "sgns_drive")
+        self.claim.zero_()
+        p = self.params
+        p.shard_hi = n_sent
+        p.claim_end = n_sent
+        p.token_base = int(token_base)
+        p.epoch_base = int(epoch)
+        p.words_base = int(token_base if words_base is None else words_base)
+        _lib.check(_lib.lib().sgns_drive(p, current_stream_ptr(self.device)), "sgns_drive")
         wv = self.workers.view(torch.int64).view(self.n_workers, WORKER_DTYPE.itemsize // 8)
-        # int64 columns of sgns_worker: 8 kernel_counter, 9 words_read, 10 words_trained, 11 inputs
+        # int64 columns of sgns_worker: 8 kernel_counter, 10 words_trained, 11 inputs
         self.stats_dev[0] = wv[:, 10].sum().double()
-        self.stats_dev[1] = wv[:, 9].sum().double()
+        self.stats_dev[1] = float(n_tok)
         self.stats_dev[2] = self.loss.sum()
         self.stats_dev[3] = self.cells.sum().double()
         self.stats_dev[4] = wv[:, 11].sum().double()
@@ -504,8 +589,6 @@ class StreamingTrainer:
         self.stats_host.copy_(self.stats_dev, non_blocking=True)
         torch.cuda.current_stream(self.device).synchronize()
         s = self.stats_host.numpy()
-        frac = 1.0 - float(self.shared[0].item()) / (self.total_x_epochs + 1.0)
-        self.alpha = self.alpha0_eff * max(frac, self.config.alpha_floor_fraction)
-        self.h2d_bytes = n_tok * 4 + (n_sent + 1) * 8 + self.workers_host.numel()
-        self.d2h_bytes = self.stats_host.numel() * 8 + 8
+        self.h2d_bytes = n_tok * 4 + (n_sent + 1) * 8
+        self.d2h_bytes = self.stats_host.numel() * 8
         return int(s[0]), int(s[1]), float(s[2]), int(s[3]), int(s[4]), int(s[5])

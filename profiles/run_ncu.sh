@@ -2,7 +2,7 @@
 # ncu evidence for the fused driver kernel (run under gpurun on one B200).
 # The plain command runs first and must exit 0 before ncu touches it.
 set -e
-CMD="python bench.py --tokens 60000000 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline"
 mkdir -p gpurun_out
 $CMD > gpurun_out/ncu_plain.log 2>&1
 # 1) launch list: every kernel with its device time (cold, serialised: compare shares)

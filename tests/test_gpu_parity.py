@@ -210,7 +210,8 @@ def test_snapshot_conflicting_windows(dtype):
 
 def _run_driver(ids, off, counts, *, window, k, cap, dynamic, subsample, seed, stream_base,
                 table_len, rng, workers=1, dtype=np.float32, dim=4, epochs=1, update=False,
-                model=None, trace_cap=None, loss_every=100, refresh=None, alpha0=0.025):
+                model=None, trace_cap=None, loss_every=100, refresh=None, alpha0=0.025,
+                schedule="static"):
     P = _pkg()
     from paper_1604_04661_b200.corpus import EncodedCorpus, keep_probabilities
     from paper_1604_04661_b200.model import DeviceModel
@@ -219,7 +220,8 @@ def _run_driver(ids, off, counts, *, window, k, cap, dynamic, subsample, seed, s
     cfg = P.TrainingConfig(dim=dim, window=window, negatives=k, batch_cap=cap, dynamic_window=dynamic,
                            subsample=subsample, seed=seed, epochs=epochs, rng=rng, workers=workers,
                            float64=dtype == np.float64, table_length=table_len, min_count=1,
-                           loss_sample_every=loss_every, alpha_refresh_words=refresh, alpha0=alpha0)
+                           loss_sample_every=loss_every, alpha_refresh_words=refresh, alpha0=alpha0,
+                           schedule=schedule)
     dm = model if model is not None else DeviceModel.empty(len(counts), dim, dtype)
     corpus = DeviceCorpus(enc)
     sampler = DeviceSampler(counts, rng, table_len)
@@ -320,3 +322,72 @@ def test_driver_train_f32_close_to_reference(name):
     np.testing.assert_allclose(stats.loss_by_epoch, g[f"{name}_loss"], rtol=5e-3)
     err = np.abs(model.input_vectors - g[f"{name}_min"]).max()
     assert err < 5e-3 * np.abs(g[f"{name}_min"]).max()
+
+
+def _oracle_philox(syn_ids, off, counts, alias, *, W, epochs, update, m_in=None, m_out=None,
+                   loss_every=0, trace_cap=0, window=5, k=5, cap=16, sub=1e-3, seed=9):
+    O = _oracle()
+    from paper_1604_04661_b200.corpus import keep_probabilities
+    from paper_1604_04661_b200.model import SIGMOID_TABLE_F32
+    keep = keep_probabilities(counts, int(counts.sum()), sub)
+    if m_in is None:
+        m_in = np.zeros((len(counts), 4), np.float32)
+        m_out = m_in.copy()
+    run = O.OracleRun(syn_ids, off, m_in, m_out, keep_probs=keep, window=window, negatives=k,
+                      batch_cap=cap, dynamic=True, seed=seed, alpha0=0.025, floor_frac=1e-4,
+                      total_x_epochs=float(off[-1]) * epochs, epochs=epochs, loss_every=loss_every,
+                      n_workers=W, rng_mode="philox", alias=alias, sig_table=SIGMOID_TABLE_F32,
+                      trace_cap=trace_cap, update=update, position_mode=True)
+    run.run_to_completion()
+    return run
+
+
+@pytest.mark.parametrize("workers", [1, 300])
+def test_fast_driver_windows_match_oracle(workers):
+    """Dynamic schedule (sgns_fast.cuh): the multiset of (sentence, epoch, target, inputs,
+    negatives, alpha) records equals the oracle's for any worker count (position-keyed draws,
+    position-based alpha)."""
+    from paper_1604_04661_b200.synthetic import make_planted_corpus
+    syn = make_planted_corpus(30_000, 400, n_clusters=4, cluster_size=5, sentence_len=37, seed=6)
+    ids, off, counts = syn.encoded.ids, syn.encoded.offsets, syn.vocab.counts
+    cap = len(ids) * 2 * 2 + 10
+    run, sampler = _run_driver(ids, off, counts, window=5, k=5, cap=6, dynamic=True, subsample=1e-3,
+                               seed=9, stream_base=0, table_len=None, rng="philox", workers=workers,
+                               epochs=2, trace_cap=cap, schedule="dynamic")
+    assert run.dynamic
+    got, got_alpha = run.trace_records()
+    orc = _oracle_philox(ids, off, counts, sampler.host_alias, W=1, epochs=2, update=False,
+                         trace_cap=cap, cap=6)
+    exp, exp_alpha = orc.worker_trace(0)
+    assert got.shape == exp.shape
+    key = lambda a, al: np.lexsort(np.column_stack([a, al.view(np.int64)]).T[::-1])
+    gi, ei = key(got, got_alpha), key(exp, exp_alpha)
+    assert np.array_equal(got[gi], exp[ei])
+    assert np.array_equal(got_alpha[gi], exp_alpha[ei])
+    assert run.words_read == orc.workers[0].words_read
+    assert run.words_trained == orc.workers[0].words_trained
+
+
+def test_fast_driver_single_worker_trains_like_oracle():
+    """One worker, dynamic schedule: same windows in the same order -> fp32 model within
+    accumulated rounding of the oracle's float64-accumulating restatement; loss within 1e-3."""
+    P = _pkg()
+    from paper_1604_04661_b200.synthetic import make_planted_corpus
+    from paper_1604_04661_b200.model import DeviceModel
+    O = _oracle()
+    syn = make_planted_corpus(30_000, 400, n_clusters=4, cluster_size=5, sentence_len=37, seed=7)
+    ids, off, counts = syn.encoded.ids, syn.encoded.offsets, syn.vocab.counts
+    V, D = len(counts), 64
+    base = O.init_model(V, D, 3).astype(np.float32)
+    dm = DeviceModel.from_host(P.EmbeddingModel(base.copy(), np.zeros_like(base)))
+    run, sampler = _run_driver(ids, off, counts, window=5, k=5, cap=16, dynamic=True, subsample=1e-3,
+                               seed=9, stream_base=0, table_len=None, rng="philox", workers=1,
+                               epochs=2, update=True, model=dm, dim=D, loss_every=3, trace_cap=0,
+                               schedule="dynamic")
+    m_in, m_out = base.copy(), np.zeros_like(base)
+    orc = _oracle_philox(ids, off, counts, sampler.host_alias, W=1, epochs=2, update=True,
+                         m_in=m_in, m_out=m_out, loss_every=3)
+    got = dm.to_host()
+    np.testing.assert_allclose(run.loss_by_epoch(), orc.stats()[2], rtol=1e-3)
+    assert np.abs(got.input_vectors - m_in).max() < 1e-3 * np.abs(m_in).max()
+    assert np.abs(got.output_vectors - m_out).max() < 1e-3 * np.abs(m_out).max()
