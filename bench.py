@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--config", choices=["large", "micro"], default="large",
+                    help="large: configs[3] (headline); micro: configs[1] isolated minibatch kernel sweep")
     return ap.parse_args()
 
 
@@ -211,10 +213,80 @@ def config_block(args, world):
 
 
 # --------------------------------------------------------------- GPU leg ----
+def micro_bench(args):
+    """BASELINE.json configs[1]: sgns_update_windows on packed windows, snapshot mode.
+
+    V = 100,000 fixed random rows ~ N(0, d^-1/2) (1% of rows x4 to hit the table clamps),
+    inputs and targets ~ Zipf(1.0) over rows, negatives ~ Zipf^0.75 rejecting the target,
+    full windows (m = 2w; w = 10 uses one chunk of 20 = batch_cap >= 20 on both sides),
+    alpha = 0.025.  One JSON line per shape; algorithmic bytes 2(m+K+1)d4 per window.
+    """
+    import torch
+    from paper_1604_04661_b200.kernel_batched import DeviceWindowBatch, WindowBatch, update_windows
+    from paper_1604_04661_b200.model import DeviceModel, EmbeddingModel
+    torch.cuda.set_device(0)
+    peak, peak_kind = measured_peaks()
+    V = 100_000
+    shapes = [(4096, 300, 5, 5), (16384, 300, 5, 5), (65536, 300, 5, 5), (65536, 100, 5, 5),
+              (65536, 200, 5, 5), (65536, 300, 2, 5), (65536, 300, 10, 5), (65536, 300, 5, 10),
+              (65536, 300, 5, 15), (65536, 100, 10, 15)]
+    rng = np.random.default_rng(args.seed)
+    ranks = np.arange(1, V + 1, dtype=np.float64)
+    pz = 1.0 / ranks
+    pz /= pz.sum()
+    pn = pz ** 0.75
+    pn /= pn.sum()
+    for n_win, d, w, k in shapes:
+        sig = d ** -0.25
+        base_in = (rng.normal(size=(V, d)) * sig).astype(np.float32)
+        base_out = (rng.normal(size=(V, d)) * sig).astype(np.float32)
+        hot = rng.choice(V, V // 100, replace=False)
+        base_in[hot] *= 4
+        m = 2 * w
+        ins = rng.choice(V, size=(n_win, m), p=pz).astype(np.int32)
+        tgt = rng.choice(V, size=n_win, p=pz).astype(np.int32)
+        negs = rng.choice(V, size=(n_win, k), p=pn).astype(np.int32)
+        bad = negs == tgt[:, None]
+        while bad.any():
+            negs[bad] = rng.choice(V, size=int(bad.sum()), p=pn)
+            bad = negs == tgt[:, None]
+        wb = WindowBatch(np.arange(0, n_win * m + 1, m, dtype=np.int32), ins.ravel(),
+                         np.concatenate([tgt[:, None], negs], axis=1).astype(np.int32))
+        dwb = DeviceWindowBatch(wb)
+        src = DeviceModel.from_host(EmbeddingModel(base_in, base_out))
+        dst = src.clone()
+        st = torch.cuda.current_stream()
+        for _ in range(args.warmup):
+            update_windows(dst, dwb, 0.025, src=src)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+        for i in range(args.steps):
+            flush.add_(1.0)  # 256 MB write between launches: L2 flushed
+            ev[i][0].record(st)
+            update_windows(dst, dwb, 0.025, src=src)
+            ev[i][1].record(st)
+        torch.cuda.synchronize()
+        t = float(np.mean([a.elapsed_time(b) for a, b in ev])) / 1e3
+        by = 2.0 * (m + k + 1) * d * 4 * n_win
+        fl = 6.0 * m * (k + 1) * d * n_win
+        print(json.dumps({"mode": "micro", "n_windows": n_win, "dim": d, "window": w, "negatives": k,
+                          "inputs_per_window": m, "us_per_launch": t * 1e6,
+                          "windows_per_sec": n_win / t, "alg_GBps": by / t / 1e9,
+                          "frac_of_peak": by / t / 1e9 / peak, "peak": peak, "peak_source": peak_kind,
+                          "GFLOPs": fl / t / 1e9, "l2": "flushed (256 MB write) before every launch"}),
+              flush=True)
+        del src, dst, dwb, flush
+        torch.cuda.empty_cache()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference_arm(args)
+        return
+    if args.config == "micro":
+        micro_bench(args)
         return
     import torch
     import torch.distributed as dist

@@ -11,7 +11,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_NAME = "libsgns_b200.so"
-LIB_PATH = os.path.join(HERE, LIB_NAME)
+LIB_PATH = os.environ.get("SGNS_LIB_OVERRIDE") or os.path.join(HERE, LIB_NAME)  # override: experiments
 
 SGNS_F32, SGNS_F64 = 0, 1
 SIGMOID_TABLE, SIGMOID_EXACT = 0, 1

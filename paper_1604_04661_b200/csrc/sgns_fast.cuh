@@ -105,25 +105,42 @@ __device__ __forceinline__ bool first_unit(const int *bw_s, int nk, int cap, Uni
   return false;
 }
 
-// Candidate negative draws of one unit: lane j evaluates attempt (attempt0 + j).
-__device__ __forceinline__ int neg_candidate(const FastArgs &p, uint64_t tok, uint32_t ep, int ch,
-                                             uint32_t a) {
+// Candidate negative draws of one unit: lane j evaluates attempt (attempt0 + j).  The
+// alias-table loads are returned raw and only combined at use time, so a prefetched
+// candidate keeps its two loads in flight while the current window computes.
+struct NegCand {
+  uint32_t bucket, coin, thr;
+  int alias;
+  __device__ __forceinline__ int word() const { return coin < thr ? (int)bucket : alias; }
+};
+__device__ __forceinline__ NegCand neg_candidate(const FastArgs &p, uint64_t tok, uint32_t ep, int ch,
+                                                 uint32_t a) {
   const uint4 o = philox_tok(tok, ep, kTagNeg | ((uint32_t)(ch & 0xFF) << 16) | ((a >> 1) & 0xFFFFu),
                              p.key0, p.key1);
-  const uint32_t bw = (a & 1) ? o.z : o.x, coin = (a & 1) ? o.w : o.y;
-  const uint32_t bucket = (uint32_t)(((uint64_t)bw * (uint64_t)p.vocab) >> 32);
-  return coin < __ldg(p.alias_thr + bucket) ? (int)bucket : __ldg(p.alias_idx + bucket);
+  NegCand c;
+  const uint32_t bw = (a & 1) ? o.z : o.x;
+  c.coin = (a & 1) ? o.w : o.y;
+  c.bucket = (uint32_t)(((uint64_t)bw * (uint64_t)p.vocab) >> 32);
+  c.thr = __ldg(p.alias_thr + c.bucket);
+  c.alias = __ldg(p.alias_idx + c.bucket);
+  return c;
+}
+__device__ __forceinline__ NegCand no_candidate() {
+  NegCand c;
+  c.bucket = 0; c.coin = 0; c.thr = 0; c.alias = -1;  // word() == -1
+  return c;
 }
 
 // Accept the first k_neg candidates != target (kernel_batched.py:57-66 semantics, with
 // the attempt sequence of the oracle's philox restatement); writes ids_s[mc+1 ...].
-__device__ __forceinline__ void select_negatives(const FastArgs &p, int cand, uint64_t tok, uint32_t ep,
+__device__ __forceinline__ void select_negatives(const FastArgs &p, NegCand cnd, uint64_t tok, uint32_t ep,
                                                  int ch, int target, int *ids_s, int mc, int lane) {
   const unsigned lt = (1u << lane) - 1u;
   int need = p.k_neg;
   uint32_t attempt = 0;
   int span = min(32, p.k_neg + 2);
   while (true) {
+    const int cand = cnd.word();
     const bool ok = lane < span && cand != target;
     const unsigned mask = __ballot_sync(0xffffffffu, ok);
     const int avail = __popc(mask);
@@ -134,12 +151,15 @@ __device__ __forceinline__ void select_negatives(const FastArgs &p, int cand, ui
     if (need == 0) break;
     attempt += (uint32_t)span;  // every candidate of this span was consumed
     span = min(32, need + 2);
-    cand = lane < span ? neg_candidate(p, tok, ep, ch, attempt + lane) : -1;
+    cnd = lane < span ? neg_candidate(p, tok, ep, ch, attempt + lane) : no_candidate();
   }
 }
 
+#ifndef SGNS_FAST_MAXNREG
+#define SGNS_FAST_MAXNREG 128
+#endif
 template <int NS, int NCH, int K1R, bool EXACT_K>
-__global__ void __launch_bounds__(256, 2) drive_fast_kernel(FastArgs p) {
+__global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
   constexpr int NV = 8;
   extern __shared__ __align__(16) unsigned char smem[];
   float *sig_s = reinterpret_cast<float *>(smem);
@@ -260,7 +280,7 @@ __global__ void __launch_bounds__(256, 2) drive_fast_kernel(FastArgs p) {
       const int target = kept_s[u.pos];
       if (lane == 0) ids_s[u.mc] = target;
       const uint64_t tok = (uint64_t)(p.token_base + lo_t + koff_s[u.pos]);
-      const int cand = lane < min(32, p.k_neg + 2) ? neg_candidate(p, tok, ep, u.ch, lane) : -1;
+      const NegCand cand = lane < min(32, p.k_neg + 2) ? neg_candidate(p, tok, ep, u.ch, lane) : no_candidate();
       select_negatives(p, cand, tok, ep, u.ch, target, ids_s, u.mc, lane);
       __syncwarp();
       for (int r = lane; r < u.mc + k1; r += 32) roff_b[r] = (uint32_t)ids_s[r] * (uint32_t)ld;
@@ -296,7 +316,7 @@ __global__ void __launch_bounds__(256, 2) drive_fast_kernel(FastArgs p) {
       // next unit + its negative candidates (alias loads in flight during u's math)
       Unit nx;
       have = next_unit(bw_s, nk, p.cap, u, nx);
-      int cand_n = -1;
+      NegCand cand_n = no_candidate();
       uint64_t tok_n = 0;
       if (have) {
         tok_n = (uint64_t)(p.token_base + lo_t + koff_s[nx.pos]);

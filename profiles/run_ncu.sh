@@ -9,5 +9,5 @@ $CMD > gpurun_out/ncu_plain.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 # 2) full set on one warm drive_kernel launch (skip the 3 warm-up launches)
-ncu --set full --clock-control none --import-source on -k regex:drive_kernel -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:drive_ -s 3 -c 1 \
     -o gpurun_out/prof_drive $CMD > gpurun_out/ncu_full.log 2>&1
