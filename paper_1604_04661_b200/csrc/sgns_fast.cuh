@@ -346,52 +346,65 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
       cp_async_wait_all();
       __syncwarp();
 
-      // scores, errors, dA
+      // scores, errors, dA -- inputs in pairs so one transposed butterfly (16 values,
+      // 5 serial shuffle stages) reduces both inputs' scores
       const float2 alpha2 = make_float2(alpha, alpha);
-      for (int i = 0; i < m; ++i) {
-        float2 a[NS];
+      for (int i = 0; i < m; i += 2) {
+        const bool two = i + 1 < m;
+        float pp[2 * NV];
 #pragma unroll
-        for (int j = 0; j < NS; ++j)
-          a[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + 2 * (lane + 32 * j))
-                            : f2zero();
-        float pp[NV];
+        for (int h = 0; h < 2; ++h) {
+          const int ii = two ? i + h : i;
+          float2 a[NS];
 #pragma unroll
-        for (int k = 0; k < NV; ++k) {
-          if (k < K1R) {
-            float2 acc = __fmul2_rn(a[0], c_reg[k][0]);
+          for (int j = 0; j < NS; ++j)
+            a[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)ii * ld + 2 * (lane + 32 * j))
+                              : f2zero();
 #pragma unroll
-            for (int j = 1; j < NS; ++j) acc = __ffma2_rn(a[j], c_reg[k][j], acc);
-            pp[k] = acc.x + acc.y;
-          } else {
-            pp[k] = 0.f;
+          for (int k = 0; k < NV; ++k) {
+            if (k < K1R) {
+              float2 acc = __fmul2_rn(a[0], c_reg[k][0]);
+#pragma unroll
+              for (int j = 1; j < NS; ++j) acc = __ffma2_rn(a[j], c_reg[k][j], acc);
+              pp[h * NV + k] = acc.x + acc.y;
+            } else {
+              pp[h * NV + k] = 0.f;
+            }
           }
         }
-        const float sc = transpose_reduce<NV>(pp, lane);
+        // value v = h * 8 + k lands on lanes 2v, 2v + 1
+        const float sc = transpose_reduce<2 * NV>(pp, lane);
+        const int v = reduced_index<2 * NV>(lane);
+        const int hk = v >> 3, kk = v & 7;
         float er = 0.f, es = 0.f;
-        if (my_k < k1) {
-          cell_error<float>(sc, my_k, alpha, false, sig_s, er, es);
-          if (leader) {
-            e_s[i * K1R + my_k] = es;
+        if (kk < k1 && (hk == 0 || two)) {
+          cell_error_f32(sc, kk, alpha, sig_s, er, es);
+          if ((lane & 1) == 0) {
+            e_s[(i + hk) * K1R + kk] = es;
             if (want) {
-              loss += softplus(my_k == 0 ? -(double)sc : (double)sc);
+              loss += softplus(kk == 0 ? -(double)sc : (double)sc);
               cells += 1;
             }
           }
         }
-        float2 d[NS];
 #pragma unroll
-        for (int k = 0; k < K1R; ++k) {
-          const float ek = __shfl_sync(0xffffffffu, er, group_leader<NV>(k));
-          const float2 ek2 = make_float2(ek, ek);
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !two) break;
+          float2 d[NS];
+#pragma unroll
+          for (int k = 0; k < K1R; ++k) {
+            const float ek = __shfl_sync(0xffffffffu, er, 2 * (h * NV + k));
+            const float2 ek2 = make_float2(ek, ek);
+#pragma unroll
+            for (int j = 0; j < NS; ++j)
+              d[j] = k == 0 ? __fmul2_rn(ek2, c_reg[0][j]) : __ffma2_rn(ek2, c_reg[k][j], d[j]);
+          }
+          float *dst = p.mv.in_dst + off_s[i + h];
 #pragma unroll
           for (int j = 0; j < NS; ++j)
-            d[j] = k == 0 ? __fmul2_rn(ek2, c_reg[0][j]) : __ffma2_rn(ek2, c_reg[k][j], d[j]);
+            if (slot_ok(j))
+              atomicAdd(reinterpret_cast<float2 *>(dst + 2 * (lane + 32 * j)), __fmul2_rn(d[j], alpha2));
         }
-        float *dst = p.mv.in_dst + off_s[i];
-#pragma unroll
-        for (int j = 0; j < NS; ++j)
-          if (slot_ok(j))
-            atomicAdd(reinterpret_cast<float2 *>(dst + 2 * (lane + 32 * j)), __fmul2_rn(d[j], alpha2));
       }
       // C registers are free: finish u+1's negatives and start loading its output rows
       // bit (8 k + k') of lo_bits (k < 4) / hi_bits (k >= 4): out(u)[k] == out(u+1)[k']
