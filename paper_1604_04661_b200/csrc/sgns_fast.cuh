@@ -63,7 +63,7 @@ __host__ __device__ inline FastSlab fast_slab(int64_t ld, int mcap, int k1r, int
   const int idsn = mcap + k1r;
   s.rows = 0;
   s.e = round16_(int64_t(mcap) * ld * 4);
-  s.ids = s.e + round16_(int64_t(mcap) * k1r * 4);
+  s.ids = s.e + round16_(int64_t(mcap) * 8 * 4);  // error rows padded to 8 floats
   s.roff = s.ids + round16_(int64_t(2) * idsn * 4);
   s.kept = s.roff + round16_(int64_t(2) * idsn * 4);
   s.koff = s.kept + round16_(int64_t(kept_cap) * 4);
@@ -380,7 +380,7 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
         if (kk < k1 && (hk == 0 || two)) {
           cell_error_f32(sc, kk, alpha, sig_s, er, es);
           if ((lane & 1) == 0) {
-            e_s[(i + hk) * K1R + kk] = es;
+            e_s[(i + hk) * 8 + kk] = es;
             if (want) {
               loss += softplus(kk == 0 ? -(double)sc : (double)sc);
               cells += 1;
@@ -442,26 +442,14 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
         float2 acc[K1R];
 #pragma unroll
         for (int k = 0; k < K1R; ++k) acc[k] = f2zero();
-        int i = 0;
-        for (; i + 1 < m; i += 2) {
+        for (int i = 0; i < m; ++i) {
           const float2 a0 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col);
-          const float2 a1 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)(i + 1) * ld + col);
+          const float4 e03 = *reinterpret_cast<const float4 *>(e_s + i * 8);
+          const float4 e47 = *reinterpret_cast<const float4 *>(e_s + i * 8 + 4);
+          const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
 #pragma unroll
           for (int k = 0; k < K1R; ++k)
-            if (kk_ok(k)) {
-              const float e0 = e_s[i * K1R + k], e1 = e_s[(i + 1) * K1R + k];
-              acc[k] = __ffma2_rn(make_float2(e0, e0), a0, acc[k]);
-              acc[k] = __ffma2_rn(make_float2(e1, e1), a1, acc[k]);
-            }
-        }
-        if (i < m) {
-          const float2 a0 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col);
-#pragma unroll
-          for (int k = 0; k < K1R; ++k)
-            if (kk_ok(k)) {
-              const float e0 = e_s[i * K1R + k];
-              acc[k] = __ffma2_rn(make_float2(e0, e0), a0, acc[k]);
-            }
+            if (kk_ok(k)) acc[k] = __ffma2_rn(make_float2(ev[k], ev[k]), a0, acc[k]);
         }
 #pragma unroll
         for (int k = 0; k < K1R; ++k)
