@@ -456,56 +456,66 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
   cp_async_wait_all();
   __syncwarp();  // staged rows were copied in 16-byte lanes, read in 8-byte lanes
 
-  const int my_k = reduced_index<NV>(lane);
-  const bool leader = (lane & ((32 / NV) - 1)) == 0;
   const float2 alpha2 = make_float2(alpha, alpha);
-  for (int i = 0; i < m; ++i) {
-    float2 a[NS];
+  // inputs in pairs: one transposed butterfly over 16 values reduces both inputs' scores
+  for (int i = 0; i < m; i += 2) {
+    const bool two = i + 1 < m;
+    float pp[2 * NV];
 #pragma unroll
-    for (int j = 0; j < NS; ++j)
-      a[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + 2 * (lane + 32 * j))
-                        : f2zero();
-    float p[NV];
+    for (int h = 0; h < 2; ++h) {
+      const int ii = two ? i + h : i;
+      float2 a[NS];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      if (k < K1R) {
-        float2 acc = __fmul2_rn(a[0], c[k][0]);
+      for (int j = 0; j < NS; ++j)
+        a[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)ii * ld + 2 * (lane + 32 * j))
+                          : f2zero();
 #pragma unroll
-        for (int j = 1; j < NS; ++j) acc = __ffma2_rn(a[j], c[k][j], acc);
-        p[k] = acc.x + acc.y;
-      } else {
-        p[k] = 0.f;
+      for (int k = 0; k < NV; ++k) {
+        if (k < K1R) {
+          float2 acc = __fmul2_rn(a[0], c[k][0]);
+#pragma unroll
+          for (int j = 1; j < NS; ++j) acc = __ffma2_rn(a[j], c[k][j], acc);
+          pp[h * NV + k] = acc.x + acc.y;
+        } else {
+          pp[h * NV + k] = 0.f;
+        }
       }
     }
-    const float s = transpose_reduce<NV>(p, lane);
+    const float s = transpose_reduce<2 * NV>(pp, lane);
+    const int v = reduced_index<2 * NV>(lane);
+    const int hk = v >> 3, kk = v & 7;
     float er = 0.f, es = 0.f;
-    if (my_k < k1) {
-      cell_error<float>(s, my_k, alpha, exact, sig_s, er, es);
-      if (leader) {
-        e_s[i * K1R + my_k] = es;
+    if (kk < k1 && (hk == 0 || two)) {
+      if (exact) cell_error<float>(s, kk, alpha, true, sig_s, er, es);
+      else cell_error_f32(s, kk, alpha, sig_s, er, es);
+      if ((lane & 1) == 0) {
+        e_s[(i + hk) * 8 + kk] = es;
         if (want_loss) {
-          loss_acc += softplus(my_k == 0 ? -(double)s : (double)s);
+          loss_acc += softplus(kk == 0 ? -(double)s : (double)s);
           cell_acc += 1;
         }
       }
     }
-    // dA_i = alpha * sum_k err_ik C_k   (kernel_batched.py:201-210)
-    float2 d[NS];
 #pragma unroll
-    for (int k = 0; k < K1R; ++k) {
-      const float ek = __shfl_sync(0xffffffffu, er, group_leader<NV>(k));
-      const float2 ek2 = make_float2(ek, ek);
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !two) break;
+      float2 d[NS];
 #pragma unroll
-      for (int j = 0; j < NS; ++j) d[j] = k == 0 ? __fmul2_rn(ek2, c[0][j]) : __ffma2_rn(ek2, c[k][j], d[j]);
+      for (int k = 0; k < K1R; ++k) {
+        const float ek = __shfl_sync(0xffffffffu, er, 2 * (h * NV + k));
+        const float2 ek2 = make_float2(ek, ek);
+#pragma unroll
+        for (int j = 0; j < NS; ++j) d[j] = k == 0 ? __fmul2_rn(ek2, c[0][j]) : __ffma2_rn(ek2, c[k][j], d[j]);
+      }
+      float *dst = mv.in_dst + off_s[i + h];
+#pragma unroll
+      for (int j = 0; j < NS; ++j)
+        if (slot_ok(j))
+          atomicAdd(reinterpret_cast<float2 *>(dst + 2 * (lane + 32 * j)), __fmul2_rn(d[j], alpha2));
     }
-    float *dst = mv.in_dst + off_s[i];
-#pragma unroll
-    for (int j = 0; j < NS; ++j)
-      if (slot_ok(j))
-        atomicAdd(reinterpret_cast<float2 *>(dst + 2 * (lane + 32 * j)), __fmul2_rn(d[j], alpha2));
   }
   __syncwarp();
-  // dC_k = sum_i (alpha err_ik) A_i, column-outer over the staged rows (i unrolled by 2)
+  // dC_k = sum_i (alpha err_ik) A_i, column-outer over the staged rows
 #pragma unroll
   for (int j = 0; j < NS; ++j) {
     if (!slot_ok(j)) continue;
@@ -513,27 +523,14 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
     float2 acc[K1R];
 #pragma unroll
     for (int k = 0; k < K1R; ++k) acc[k] = f2zero();
-    int i = 0;
-    for (; i + 1 < m; i += 2) {
+    for (int i = 0; i < m; ++i) {
       const float2 a0 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col);
-      const float2 a1 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)(i + 1) * ld + col);
-#pragma unroll
-      for (int k = 0; k < K1R; ++k) {
-        if (kk_ok(k)) {
-          const float e0 = e_s[i * K1R + k], e1 = e_s[(i + 1) * K1R + k];
-          acc[k] = __ffma2_rn(make_float2(e0, e0), a0, acc[k]);
-          acc[k] = __ffma2_rn(make_float2(e1, e1), a1, acc[k]);
-        }
-      }
-    }
-    if (i < m) {
-      const float2 a0 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col);
+      const float4 e03 = *reinterpret_cast<const float4 *>(e_s + i * 8);
+      const float4 e47 = *reinterpret_cast<const float4 *>(e_s + i * 8 + 4);
+      const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
 #pragma unroll
       for (int k = 0; k < K1R; ++k)
-        if (kk_ok(k)) {
-          const float e0 = e_s[i * K1R + k];
-          acc[k] = __ffma2_rn(make_float2(e0, e0), a0, acc[k]);
-        }
+        if (kk_ok(k)) acc[k] = __ffma2_rn(make_float2(ev[k], ev[k]), a0, acc[k]);
     }
 #pragma unroll
     for (int k = 0; k < K1R; ++k)

@@ -186,8 +186,6 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
   auto slot_ok = [&](int j) { return j < NS - 1 || lane + 32 * j < nslot; };
   auto chunk_ok = [&](int j) { return j < NCH - 1 || lane + 32 * j < nvec; };
   auto kk_ok = [&](int k) { return EXACT_K || k < k1; };
-  const int my_k = reduced_index<NV>(lane);
-  const bool leader = (lane & ((32 / NV) - 1)) == 0;
   const int64_t off0 = p.offsets[p.shard_lo];
   const int64_t shard_tokens = p.offsets[p.shard_lo + p.n_sent] - off0;
   const int rec_len = 4 + p.cap + k1;

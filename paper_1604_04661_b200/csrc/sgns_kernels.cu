@@ -36,7 +36,7 @@ __host__ __device__ inline Slab slab_layout(int mode, int64_t elem, int64_t ld, 
   Slab s;
   s.rows = 0;
   s.e = round16((int64_t)(mode == MODE_F2 ? mcap : mcap + k1) * ld * elem);
-  s.ids = s.e + round16((int64_t)2 * mcap * k1 * elem);
+  s.ids = s.e + round16((int64_t)2 * mcap * (k1 > 8 ? k1 : 8) * elem);  // F2 rows padded to 8
   s.roff = s.ids + round16((int64_t)(mcap + k1) * 4);
   s.kept = s.roff + round16((int64_t)(mcap + k1) * 4);
   s.off = s.kept + round16((int64_t)kept_cap * 4);
