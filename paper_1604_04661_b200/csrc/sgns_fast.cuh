@@ -158,7 +158,9 @@ __device__ __forceinline__ void select_negatives(const FastArgs &p, NegCand cnd,
 #ifndef SGNS_FAST_MAXNREG
 #define SGNS_FAST_MAXNREG 128
 #endif
-template <int NS, int NCH, int K1R, bool EXACT_K>
+// FULL: the row holds exactly 32 * NS float2 slots (ld padded, e.g. 320 at d = 300), so
+// every lane owns NS whole slots and no per-slot predicate is needed.
+template <int NS, int NCH, int K1R, bool EXACT_K, bool FULL>
 __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
   constexpr int NV = 8;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -183,7 +185,7 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t ld = p.mv.ld;
   const int nvec = p.mv.nvec, nslot = 2 * nvec;
-  auto slot_ok = [&](int j) { return j < NS - 1 || lane + 32 * j < nslot; };
+  auto slot_ok = [&](int j) { return FULL || j < NS - 1 || lane + 32 * j < nslot; };
   auto chunk_ok = [&](int j) { return j < NCH - 1 || lane + 32 * j < nvec; };
   auto kk_ok = [&](int k) { return EXACT_K || k < k1; };
   const int64_t off0 = p.offsets[p.shard_lo];
@@ -375,15 +377,12 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
         const int v = reduced_index<2 * NV>(lane);
         const int hk = v >> 3, kk = v & 7;
         float er = 0.f, es = 0.f;
-        if (kk < k1 && (hk == 0 || two)) {
-          cell_error_f32(sc, kk, alpha, sig_s, er, es);
-          if ((lane & 1) == 0) {
-            e_s[(i + hk) * 8 + kk] = es;
-            if (want) {
-              loss += softplus(kk == 0 ? -(double)sc : (double)sc);
-              cells += 1;
-            }
-          }
+        const bool live = kk < k1 && (hk == 0 || two);
+        cell_error_f32(sc, kk, alpha, sig_s, er, es);
+        if (live) e_s[(i + hk) * 8 + kk] = es;  // both lanes of the pair hold the same value
+        if (want && live && (lane & 1) == 0) {
+          loss += softplus(kk == 0 ? -(double)sc : (double)sc);
+          cells += 1;
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {

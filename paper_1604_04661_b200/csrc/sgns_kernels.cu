@@ -678,10 +678,10 @@ static void fill_drive_args(DriveArgs<T> &a, const sgns_drive_params *p) {
 }
 
 // ------------------------------------------------------------ fast path ----
-template <int NS, int K1R, bool EXACT>
+template <int NS, int K1R, bool EXACT, bool FULL>
 static int launch_fast_t(FastArgs a, int wpb_req, cudaStream_t st, int *resident) {
   constexpr int NCH = (NS + 1) / 2;
-  auto kern = drive_fast_kernel<NS, NCH, K1R, EXACT>;
+  auto kern = drive_fast_kernel<NS, NCH, K1R, EXACT, FULL>;
   const FastSlab L = fast_slab(a.mv.ld, std::min(a.cap, 2 * a.window), K1R, a.kept_cap);
   int wpb = 0, bps = 0;
   int rc = choose_wpb(kern, table_bytes(4), L.total, &wpb, &bps);
@@ -701,8 +701,12 @@ static int launch_fast_t(FastArgs a, int wpb_req, cudaStream_t st, int *resident
 
 template <int NS>
 static int fast_ns(FastArgs a, int wpb, cudaStream_t st, int *res) {
-  if (a.k_neg + 1 == 6) return launch_fast_t<NS, 6, true>(a, wpb, st, res);
-  return launch_fast_t<NS, 8, false>(a, wpb, st, res);
+  const bool full = a.mv.ld == 64 * NS;  // 32 lanes x NS float2 slots exactly
+  if (a.k_neg + 1 == 6)
+    return full ? launch_fast_t<NS, 6, true, true>(a, wpb, st, res)
+                : launch_fast_t<NS, 6, true, false>(a, wpb, st, res);
+  return full ? launch_fast_t<NS, 8, false, true>(a, wpb, st, res)
+              : launch_fast_t<NS, 8, false, false>(a, wpb, st, res);
 }
 
 static bool fast_eligible(const sgns_drive_params *p) {
