@@ -391,7 +391,7 @@ def main():
     achieved = bytes_step / avg_kernel_s / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
-                "kernel": "drive_kernel<float,MODE_F2,NS=5,NCH=3,K1R=6,PHILOX>",
+                "kernel": "drive_fast_kernel<NS=5,NCH=3,K1R=6,EXACT_K> (dynamic schedule, Philox)",
                 "algorithmic_bytes_per_launch": bytes_step,
                 "gflops": flops_step / avg_kernel_s / 1e9,
                 "avg_launch_ms": avg_kernel_s * 1000.0,

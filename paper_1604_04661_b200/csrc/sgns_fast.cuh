@@ -192,7 +192,7 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
   const int64_t shard_tokens = p.offsets[p.shard_lo + p.n_sent] - off0;
   const int rec_len = 4 + p.cap + k1;
 
-  long long chunks = 0, trained = 0, inputs = 0;
+  long long chunks = 0, trained = 0, inputs = 0, read = 0;
   double loss = 0.0;
   long long cells = 0;
   int loss_epoch = -1;
@@ -211,6 +211,7 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
       continue;
     }
     const uint32_t ep = p.epoch_base + (uint32_t)epoch;
+    read += n;
     // alpha from the sentence's words-read position (update_alpha, trainer.py:122-132)
     const double pos_words = (double)(p.words_base + (int64_t)epoch * shard_tokens + (lo_t - off0));
     double frac = 1.0 - pos_words / (p.total_x_epochs + 1.0);
@@ -486,6 +487,7 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
     sgns_worker &o = p.workers[wid];
     o.kernel_counter += chunks;
     o.words_trained += trained;
+    o.words_read += read;
     o.inputs += inputs;
   }
 }
