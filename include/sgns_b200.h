@@ -39,7 +39,9 @@ enum {
   SGNS_E_ARG = -1,       /* bad argument (null pointer, size, mode) */
   SGNS_E_SHAPE = -2,     /* dim / window / K / batch_cap outside the supported envelope */
   SGNS_E_SMEM = -3,      /* per-warp staging does not fit in shared memory */
-  SGNS_E_DEVICE = -4     /* device-side validation failed (see sgns_error_string) */
+  SGNS_E_DEVICE = -4,    /* device-side validation failed (see sgns_error_string) */
+  SGNS_E_IO = -5,        /* corpus file could not be opened / mapped */
+  SGNS_E_EMPTY = -6      /* no token reaches min_count (EmptyVocabularyError) */
 };
 
 enum { SGNS_F32 = 0, SGNS_F64 = 1 };
@@ -141,6 +143,25 @@ int sgns_build_alias(const int64_t *h_counts, int64_t vocab, double power,
 /* Occupancy-derived worker count: resident warps of the driver kernel. */
 int sgns_resident_workers(int32_t dtype, int32_t dim, int32_t window, int32_t k_neg,
                           int32_t batch_cap, int32_t max_sentence, int32_t *out_workers);
+
+/* ---- host-side corpus ingestion (sgns_ingest.cpp) ----
+ * Same vocabulary / encoding as build_vocab(read_tokens(path), min_count)
+ * (corpus.py:86-105, :268-272) and encode_corpus(path, vocab) (corpus.py:275-311),
+ * multithreaded over an mmap of the file. */
+typedef struct sgns_vocab sgns_vocab;
+typedef struct sgns_encoded sgns_encoded;
+int sgns_vocab_build(const char *path, int32_t min_count, int32_t threads, sgns_vocab **out,
+                     int64_t *vocab_size, int64_t *tokens_bytes);
+int sgns_vocab_from_tokens(const char *blob, const int64_t *token_offsets /* n + 1 */,
+                           const int64_t *counts /* may be NULL */, int64_t n, sgns_vocab **out);
+int sgns_vocab_export(const sgns_vocab *v, char *blob, int64_t *token_offsets /* n + 1 */,
+                      int64_t *counts);
+void sgns_vocab_free(sgns_vocab *v);
+int sgns_encode(const sgns_vocab *v, const char *path, int32_t max_sentence, int32_t threads,
+                sgns_encoded **out, int64_t *n_tokens, int64_t *n_sentences);
+int sgns_encoded_export(const sgns_encoded *e, int32_t *ids, int64_t *offsets /* n_sentences + 1 */,
+                        int64_t *sentence_bytes);
+void sgns_encoded_free(sgns_encoded *e);
 
 const char *sgns_error_string(int32_t code);
 int sgns_abi_version(void);

@@ -80,6 +80,20 @@ def lib() -> C.CDLL:
     L.sgns_build_alias.argtypes = [P, I64, F64, P, P]
     L.sgns_resident_workers.restype = C.c_int
     L.sgns_resident_workers.argtypes = [I32, I32, I32, I32, I32, I32, C.POINTER(I32)]
+    L.sgns_vocab_build.restype = C.c_int
+    L.sgns_vocab_build.argtypes = [C.c_char_p, I32, I32, C.POINTER(P), C.POINTER(I64), C.POINTER(I64)]
+    L.sgns_vocab_from_tokens.restype = C.c_int
+    L.sgns_vocab_from_tokens.argtypes = [P, P, P, I64, C.POINTER(P)]
+    L.sgns_vocab_export.restype = C.c_int
+    L.sgns_vocab_export.argtypes = [P, P, P, P]
+    L.sgns_vocab_free.restype = None
+    L.sgns_vocab_free.argtypes = [P]
+    L.sgns_encode.restype = C.c_int
+    L.sgns_encode.argtypes = [P, C.c_char_p, I32, I32, C.POINTER(P), C.POINTER(I64), C.POINTER(I64)]
+    L.sgns_encoded_export.restype = C.c_int
+    L.sgns_encoded_export.argtypes = [P, P, P, P]
+    L.sgns_encoded_free.restype = None
+    L.sgns_encoded_free.argtypes = [P]
     L.sgns_struct_sizes.restype = C.c_int
     L.sgns_struct_sizes.argtypes = [C.POINTER(I32), C.POINTER(I32)]
     if L.sgns_abi_version() != 1:
@@ -95,7 +109,8 @@ def lib() -> C.CDLL:
 
 EXPORTED = ("sgns_update_windows", "sgns_drive", "sgns_init_model", "sgns_expand_slots",
             "sgns_build_alias", "sgns_resident_workers", "sgns_error_string", "sgns_abi_version",
-            "sgns_struct_sizes")
+            "sgns_struct_sizes", "sgns_vocab_build", "sgns_vocab_from_tokens", "sgns_vocab_export",
+            "sgns_vocab_free", "sgns_encode", "sgns_encoded_export", "sgns_encoded_free")
 
 
 class SgnsError(RuntimeError):

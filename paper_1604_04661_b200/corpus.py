@@ -279,3 +279,76 @@ def split_by_tokens(offsets: np.ndarray, sent_lo: int, sent_hi: int,
         bounds[k] = prev
     bounds[parts] = sent_hi
     return [(int(bounds[i]), int(bounds[i + 1])) for i in range(parts)]
+
+
+# ---------------------------------------------------------------- native ingestion ----
+def _threads(threads: int | None) -> int:
+    import os
+    return threads if threads else max(1, len(os.sched_getaffinity(0)))
+
+
+def _native_vocab_to_python(L, handle, n: int, nbytes: int) -> Vocabulary:
+    import ctypes as C
+    blob = C.create_string_buffer(max(nbytes, 1))
+    offs = np.empty(n + 1, dtype=np.int64)
+    counts = np.empty(n, dtype=np.int64)
+    if L.sgns_vocab_export(handle, blob, offs.ctypes.data, counts.ctypes.data) != 0:
+        raise RuntimeError("sgns_vocab_export failed")
+    raw = blob.raw
+    tokens = [raw[offs[i]:offs[i + 1]].decode("utf-8") for i in range(n)]
+    return Vocabulary(tokens, counts, {t: i for i, t in enumerate(tokens)}, int(counts.sum()))
+
+
+def build_vocab_file(path: str, min_count: int, threads: int | None = None) -> Vocabulary:
+    """build_vocab(read_tokens(path), min_count), computed by the multithreaded C++ scanner."""
+    import ctypes as C
+    from . import _lib
+    L = _lib.lib()
+    h, n, nb = C.c_void_p(), C.c_int64(), C.c_int64()
+    rc = L.sgns_vocab_build(path.encode(), min_count, _threads(threads), C.byref(h), C.byref(n), C.byref(nb))
+    if rc == -6:
+        raise EmptyVocabularyError(f"no token appears at least min_count={min_count} times")
+    if rc == -5:
+        raise FileNotFoundError(path)
+    if rc != 0:
+        raise ValueError(f"sgns_vocab_build failed ({rc})")
+    try:
+        return _native_vocab_to_python(L, h, n.value, nb.value)
+    finally:
+        L.sgns_vocab_free(h)
+
+
+def encode_corpus_file(path: str, vocab: Vocabulary, max_sentence: int = MAX_SENTENCE_TOKENS,
+                       threads: int | None = None) -> EncodedCorpus:
+    """encode_corpus(path, vocab), computed by the multithreaded C++ scanner."""
+    import ctypes as C
+    from . import _lib
+    L = _lib.lib()
+    enc_tokens = [t.encode("utf-8") for t in vocab.tokens]
+    offs = np.zeros(len(enc_tokens) + 1, dtype=np.int64)
+    offs[1:] = np.cumsum([len(t) for t in enc_tokens])
+    blob = b"".join(enc_tokens)
+    blob_buf = C.create_string_buffer(blob, max(len(blob), 1))
+    counts = np.ascontiguousarray(vocab.counts, dtype=np.int64)
+    vh = C.c_void_p()
+    if L.sgns_vocab_from_tokens(C.addressof(blob_buf), offs.ctypes.data, counts.ctypes.data,
+                                len(enc_tokens), C.byref(vh)) != 0:
+        raise ValueError("sgns_vocab_from_tokens failed")
+    try:
+        eh, nt, ns = C.c_void_p(), C.c_int64(), C.c_int64()
+        rc = L.sgns_encode(vh, path.encode(), max_sentence, _threads(threads), C.byref(eh),
+                           C.byref(nt), C.byref(ns))
+        if rc == -5:
+            raise FileNotFoundError(path)
+        if rc != 0:
+            raise ValueError(f"sgns_encode failed ({rc})")
+        try:
+            ids = np.empty(nt.value, dtype=np.int32)
+            offsets = np.empty(ns.value + 1, dtype=np.int64)
+            sbytes = np.empty(ns.value, dtype=np.int64)
+            L.sgns_encoded_export(eh, ids.ctypes.data, offsets.ctypes.data, sbytes.ctypes.data)
+        finally:
+            L.sgns_encoded_free(eh)
+    finally:
+        L.sgns_vocab_free(vh)
+    return EncodedCorpus(ids, offsets, sbytes)

@@ -817,6 +817,8 @@ const char *sgns_error_string(int32_t code) {
     case SGNS_E_SHAPE: return "shape outside the supported envelope (dim <= 1024 f32 / 512 f64, k+1 <= 32)";
     case SGNS_E_SMEM: return "per-warp staging does not fit in 227 KB of shared memory";
     case SGNS_E_DEVICE: return "device-side validation failed";
+    case SGNS_E_IO: return "corpus file could not be opened";
+    case SGNS_E_EMPTY: return "no token appears at least min_count times";
   }
   if (code > 0) return cudaGetErrorString((cudaError_t)code);
   return "unknown error";

@@ -220,8 +220,9 @@ def distributed_train(corpus_path: str | None, config: TrainingConfig, policy: S
     else:
         if corpus_path is None:
             raise ValueError("need a corpus path or a prebuilt (vocab, corpus) pair")
-        vocab = build_vocab(read_tokens(corpus_path), config.min_count)
-        encoded = encode_corpus(corpus_path, vocab)
+        from .corpus import build_vocab_file, encode_corpus_file
+        vocab = build_vocab_file(corpus_path, config.min_count)
+        encoded = encode_corpus_file(corpus_path, vocab)
     nodes = transport.nodes
     policy = policy.resolve(vocab.size)
     shards = partition_corpus(encoded, nodes)

@@ -469,10 +469,12 @@ def train_encoded(vocab: Vocabulary, encoded: EncodedCorpus, config: TrainingCon
 
 
 def train(corpus_path: str, config: TrainingConfig, progress: bool = False):
-    """Build the vocabulary, encode the corpus, and train a fresh model on the GPU."""
+    """Build the vocabulary, encode the corpus (multithreaded C++ scanner, identical to
+    build_vocab/encode_corpus), and train a fresh model on the GPU."""
+    from .corpus import build_vocab_file, encode_corpus_file
     config.validate()
-    vocab = build_vocab(read_tokens(corpus_path), config.min_count)
-    encoded = encode_corpus(corpus_path, vocab)
+    vocab = build_vocab_file(corpus_path, config.min_count)
+    encoded = encode_corpus_file(corpus_path, vocab)
     model, stats = train_encoded(vocab, encoded, config, progress=progress)
     return model, vocab, stats
 

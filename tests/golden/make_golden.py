@@ -290,8 +290,44 @@ def gen_eval():
                         pairs=np.array([text]), rho=np.array([rho, used, skipped]))
 
 
+def gen_ingest():
+    """A text corpus exercising every str.split() whitespace class, universal newlines,
+    >1000-token lines, OOV-only and empty lines and an unterminated last line; the
+    reference's build_vocab(read_tokens) / encode_corpus outputs pin the C++ scanner."""
+    rng = np.random.default_rng(77)
+    words = [f"w{i}" for i in range(300)] + ["naïve", "日本語", "über", "ça", "x\u200by", "Ω", "a", "A"]
+    p = 1.0 / np.arange(1, len(words) + 1)
+    p /= p.sum()
+    seps = [" ", " ", " ", "\t", "\x0b", "\x0c", "\x1c", "\x1f", "\xa0", "\u2003", "\u3000",
+            "\x85", "\u2028", "\u205f", "  \t "]
+    ends = ["\n", "\n", "\r\n", "\r"]
+    lines = []
+    for li in range(400):
+        n = int(rng.integers(0, 40)) if li % 50 else int(rng.integers(1000, 2600))
+        toks = [words[i] for i in rng.choice(len(words), size=n, p=p)]
+        if li % 37 == 5:
+            toks = [f"oov{li}_{k}" for k in range(5)]
+        body = ""
+        for t in toks:
+            body += t + seps[int(rng.integers(len(seps)))]
+        if li % 9 == 0:
+            body = seps[int(rng.integers(len(seps)))] + body
+        lines.append(body + ends[int(rng.integers(len(ends)))])
+    text = "".join(lines) + "w1 w2 tail"  # unterminated last line
+    path = os.path.join(HERE, "ingest_corpus.txt")
+    with open(path, "w", encoding="utf-8", newline="") as fh:
+        fh.write(text)
+    voc = rc.build_vocab(rc.read_tokens(path), 2)
+    enc = rc.encode_corpus(path, voc)
+    np.savez_compressed(os.path.join(HERE, "ingest.npz"),
+                        tokens=np.array("\x00".join(voc.tokens)), counts=voc.counts,
+                        total=np.array([voc.total_tokens]), ids=enc.ids, offsets=enc.offsets,
+                        sentence_bytes=enc.sentence_bytes)
+
+
 if __name__ == "__main__":
     assert sgns.__version__
-    for fn in (gen_rng, gen_tables, gen_init, gen_kernel, gen_traces, gen_train, gen_dist, gen_eval):
+    for fn in (gen_rng, gen_tables, gen_init, gen_kernel, gen_traces, gen_train, gen_dist, gen_eval,
+               gen_ingest):
         fn()
         print("wrote", fn.__name__)
