@@ -49,6 +49,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--sync-hot-rows", type=int, default=-1,
+                    help="configs[4] sweep: average only rows [0, N) + the reference's round-robin "
+                         "chunk each step (-1: full model, configs[3])")
+    ap.add_argument("--sync-rotation", type=int, default=-1,
+                    help="rotation chunk for --sync-hot-rows (-1: the reference default, 1/20 of the cold rows)")
     ap.add_argument("--config", choices=["large", "micro"], default="large",
                     help="large: configs[3] (headline); micro: configs[1] isolated minibatch kernel sweep")
     return ap.parse_args()
@@ -209,6 +214,8 @@ def config_block(args, world):
             "tokens": args.tokens, "vocab_raw": args.vocab, "dim": DIM, "window": WINDOW,
             "negatives": NEG, "subsample": SUBSAMPLE, "period_words_per_gpu": args.period,
             "parallelism": f"dp{world}",
+            "sync": "full model every period" if args.sync_hot_rows < 0 else
+                    f"rows [0,{args.sync_hot_rows}) + round-robin chunk every period",
             "l2": "model 2.4 GB and corpus 3.2 GB exceed the 126 MB L2; no flush between steps"}
 
 
@@ -329,6 +336,19 @@ def main():
     budget = math.ceil(args.period / W)
     stream = torch.cuda.current_stream(dev)
     all_rows = np.arange(V, dtype=np.int64)
+    sync_policy = None
+    if args.sync_hot_rows >= 0:
+        from paper_1604_04661_b200.distributed import SyncPolicy, select_sync_rows
+        sync_policy = SyncPolicy(period_words=args.period, hot_rows=min(args.sync_hot_rows, V),
+                                 rotation_chunk=None if args.sync_rotation < 0 else args.sync_rotation)
+    period_index = [0]
+
+    def sync_rows():
+        if sync_policy is None:
+            return all_rows
+        rows = select_sync_rows(V, sync_policy, period_index[0])
+        period_index[0] += 1
+        return rows
     wv = run.workers.view(torch.int64).view(W, 12)
 
     def counters():
@@ -344,8 +364,9 @@ def main():
         if i is not None:
             k_ev[i][1].record(stream)
         if transport is not None:
-            transport.allreduce_average(model.m_in, all_rows, "in")
-            transport.allreduce_average(model.m_out, all_rows, "out")
+            rows = sync_rows()
+            transport.allreduce_average(model.m_in, rows, "in")
+            transport.allreduce_average(model.m_out, rows, "out")
 
     for _ in range(args.warmup):
         step()
