@@ -163,6 +163,14 @@ int sgns_encoded_export(const sgns_encoded *e, int32_t *ids, int64_t *offsets /*
                         int64_t *sentence_bytes);
 void sgns_encoded_free(sgns_encoded *e);
 
+/* ---- word2vec vector files (sgns_io.cpp) ----
+ * save_model (model.py:118-139) byte for byte: "V D\n" then per word the token, a space,
+ * and either D "%.6g" values (text) or D little-endian float32 (binary), then "\n".
+ * rows: (V, ld) float32, in device memory when rows_on_device != 0 (streamed D2H). */
+int sgns_write_vectors(const char *path, const char *tokens_blob, const int64_t *token_offsets,
+                       int64_t vocab, int32_t dim, const float *rows, int64_t ld, int32_t binary,
+                       int32_t rows_on_device);
+
 const char *sgns_error_string(int32_t code);
 int sgns_abi_version(void);
 /* sizeof(sgns_worker), sizeof(sgns_drive_params): lets bindings check their layout. */

@@ -94,6 +94,8 @@ def lib() -> C.CDLL:
     L.sgns_encoded_export.argtypes = [P, P, P, P]
     L.sgns_encoded_free.restype = None
     L.sgns_encoded_free.argtypes = [P]
+    L.sgns_write_vectors.restype = C.c_int
+    L.sgns_write_vectors.argtypes = [C.c_char_p, P, P, I64, I32, P, I64, I32, I32]
     L.sgns_struct_sizes.restype = C.c_int
     L.sgns_struct_sizes.argtypes = [C.POINTER(I32), C.POINTER(I32)]
     if L.sgns_abi_version() != 1:
@@ -110,7 +112,8 @@ def lib() -> C.CDLL:
 EXPORTED = ("sgns_update_windows", "sgns_drive", "sgns_init_model", "sgns_expand_slots",
             "sgns_build_alias", "sgns_resident_workers", "sgns_error_string", "sgns_abi_version",
             "sgns_struct_sizes", "sgns_vocab_build", "sgns_vocab_from_tokens", "sgns_vocab_export",
-            "sgns_vocab_free", "sgns_encode", "sgns_encoded_export", "sgns_encoded_free")
+            "sgns_vocab_free", "sgns_encode", "sgns_encoded_export", "sgns_encoded_free",
+            "sgns_write_vectors")
 
 
 class SgnsError(RuntimeError):

@@ -192,3 +192,124 @@ def sigmoid_table_device(dtype, device="cuda"):
     torch = _torch()
     tab = SIGMOID_TABLE_F64 if np.dtype(dtype) == np.float64 else SIGMOID_TABLE_F32
     return torch.from_numpy(tab.copy()).to(device)
+
+
+# ------------------------------------------------------------------- vector files ----
+class ModelFormatError(ValueError):
+    """Vector file does not match the expected layout (model.py:22-23)."""
+
+
+def save_model(model, vocab, path: str, binary: bool = False) -> None:
+    """Write input_vectors as a word2vec text/binary file (model.py:118-139), byte-identical.
+
+    model: EmbeddingModel (host float32/float64) or DeviceModel (float32 rows are
+    streamed device -> host by the writer)."""
+    import ctypes as C
+    if model.vocab_size != vocab.size:
+        raise ValueError(f"model has {model.vocab_size} rows but vocabulary has {vocab.size}")
+    enc = [t.encode("utf-8") for t in vocab.tokens]
+    offs = np.zeros(len(enc) + 1, dtype=np.int64)
+    offs[1:] = np.cumsum([len(t) for t in enc])
+    blob = C.create_string_buffer(b"".join(enc), max(int(offs[-1]), 1))
+    if isinstance(model, DeviceModel) and model.np_dtype == np.float32:
+        rows, ld, on_dev, keep = model.m_in.data_ptr(), model.ld, 1, model.m_in
+        import torch
+        torch.cuda.synchronize(model.m_in.device)
+    else:
+        host = model.to_host() if isinstance(model, DeviceModel) else model
+        arr = np.ascontiguousarray(host.input_vectors, dtype=np.float32)
+        rows, ld, on_dev, keep = arr.ctypes.data, arr.shape[1], 0, arr
+    rc = _lib.lib().sgns_write_vectors(path.encode(), C.addressof(blob), offs.ctypes.data, vocab.size,
+                                       model.dim, rows, ld, int(binary), on_dev)
+    del keep
+    if rc == -5:
+        raise OSError(f"cannot write {path}")
+    _lib.check(rc, "sgns_write_vectors")
+
+
+def _parse_header(line: bytes, path: str) -> tuple[int, int]:
+    try:
+        fields = line.decode("utf-8").split()
+        if len(fields) != 2:
+            raise ValueError
+        v, d = int(fields[0]), int(fields[1])
+        if v < 1 or d < 1:
+            raise ValueError
+    except (ValueError, UnicodeDecodeError):
+        raise ModelFormatError(f"{path}: malformed header {line!r}") from None
+    return v, d
+
+
+def detect_format(path: str) -> bool:
+    """True when the payload looks binary (same sniffing rule as model.py:155-172)."""
+    with open(path, "rb") as fh:
+        v, d = _parse_header(fh.readline(), path)
+        probe = fh.read(d * 16 + 64)
+    try:
+        text = probe.decode("utf-8")
+    except UnicodeDecodeError:
+        return True
+    fields = text.split()
+    if len(fields) < d + 1:
+        return len(probe) > 0
+    try:
+        [float(f) for f in fields[1:d + 1]]
+        return False
+    except ValueError:
+        return True
+
+
+def load_model(path: str, binary: bool | None = None):
+    """Read a vector file back (model.py:175-225); output_vectors come back zero."""
+    from .corpus import Vocabulary
+    if binary is None:
+        binary = detect_format(path)
+    tokens: list[str] = []
+    if binary:
+        with open(path, "rb") as fh:
+            v, d = _parse_header(fh.readline(), path)
+            data = fh.read()
+        vectors = np.empty((v, d), dtype=np.float32)
+        pos, nb = 0, 4 * d
+        for i in range(v):
+            sp = data.find(b" ", pos)
+            if sp < 0 or sp + 1 + nb > len(data):
+                raise ModelFormatError(f"{path}: truncated file at word {i} of {v}")
+            tokens.append(data[pos:sp].decode("utf-8").lstrip("\n"))
+            vectors[i] = np.frombuffer(data, dtype="<f4", count=d, offset=sp + 1)
+            pos = sp + 1 + nb
+            if pos < len(data) and data[pos:pos + 1] == b"\n":
+                pos += 1
+    else:
+        with open(path, encoding="utf-8") as fh:
+            v, d = _parse_header(fh.readline().encode("utf-8"), path)
+            vectors = np.empty((v, d), dtype=np.float32)
+            for i in range(v):
+                line = fh.readline()
+                if not line:
+                    raise ModelFormatError(f"{path}: truncated file at word {i} of {v}")
+                fields = line.rstrip("\n").split(" ")
+                if len(fields) != d + 1:
+                    raise ModelFormatError(f"{path}: dimension mismatch at word {i}: "
+                                           f"expected {d} values, got {len(fields) - 1}")
+                tokens.append(fields[0])
+                vectors[i] = [float(f) for f in fields[1:]]
+    counts = np.ones(v, dtype=np.int64)
+    vocab = Vocabulary(tokens, counts, {t: i for i, t in enumerate(tokens)}, v)
+    return EmbeddingModel(vectors, np.zeros_like(vectors)), vocab
+
+
+def save_debug(model, vocab, path: str) -> None:
+    """Both matrices losslessly (model.py:228-236)."""
+    host = model.to_host() if isinstance(model, DeviceModel) else model
+    np.savez(path, input_vectors=host.input_vectors, output_vectors=host.output_vectors,
+             tokens=np.array(vocab.tokens, dtype=object), counts=vocab.counts)
+
+
+def load_debug(path: str):
+    from .corpus import Vocabulary
+    data = np.load(path, allow_pickle=True)
+    tokens = list(data["tokens"])
+    counts = data["counts"]
+    vocab = Vocabulary(tokens, counts, {t: i for i, t in enumerate(tokens)}, int(counts.sum()))
+    return EmbeddingModel(data["input_vectors"], data["output_vectors"]), vocab

@@ -325,9 +325,28 @@ def gen_ingest():
                         sentence_bytes=enc.sentence_bytes)
 
 
+def gen_io():
+    """save_model text and binary bytes from the reference, on values that stress %.6g."""
+    rng = np.random.default_rng(31)
+    V, D = 23, 7
+    vecs = (rng.normal(size=(V, D)) * 10.0 ** rng.integers(-9, 9, size=(V, D))).astype(np.float32)
+    vecs[0, :] = [0.0, -0.0, 1e-45, 3.4e38, 123456.5, 1234567.0, 0.1]
+    toks = [f"w{i}" for i in range(V - 2)] + ["naïve", "日本語"]
+    voc = rc.Vocabulary(toks, np.arange(V, 0, -1, dtype=np.int64), {t: i for i, t in enumerate(toks)},
+                        int(np.arange(V, 0, -1).sum()))
+    model = rm.EmbeddingModel(vecs, np.zeros_like(vecs))
+    out = {"vecs": vecs, "tokens": np.array("\x00".join(toks))}
+    for binary in (False, True):
+        path = os.path.join("/tmp", f"golden_vec_{int(binary)}")
+        rm.save_model(model, voc, path, binary=binary)
+        with open(path, "rb") as fh:
+            out[f"bytes_{int(binary)}"] = np.frombuffer(fh.read(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "io.npz"), **out)
+
+
 if __name__ == "__main__":
     assert sgns.__version__
     for fn in (gen_rng, gen_tables, gen_init, gen_kernel, gen_traces, gen_train, gen_dist, gen_eval,
-               gen_ingest):
+               gen_ingest, gen_io):
         fn()
         print("wrote", fn.__name__)
