@@ -275,6 +275,49 @@ def gen_dist():
     np.savez_compressed(os.path.join(HERE, "dist.npz"), **out)
 
 
+def gen_eval_full():
+    """eval_similarity / eval_analogy of the reference on random vectors, header lines,
+    OOV words, lowercase fallback, sections and max_vocab."""
+    rng = np.random.default_rng(12)
+    V, D = 400, 24
+    toks = [f"w{i}" for i in range(V - 2)] + ["Paris", "rome"]
+    voc = rc.Vocabulary(toks, np.arange(V, 0, -1, dtype=np.int64), {t: i for i, t in enumerate(toks)}, 1)
+    vecs = rng.normal(size=(V, D)).astype(np.float32)
+    vecs[5] = 0.0  # zero row: analogy normalisation guard
+    model = rm.EmbeddingModel(vecs, np.zeros_like(vecs))
+    sim = ["word1 word2 score"]
+    for _ in range(150):
+        a, b = rng.integers(0, V, 2)
+        if a == 5 or b == 5:
+            continue
+        sim.append(f"{toks[a]} {toks[b]} {rng.uniform(0, 10):.2f}")
+    sim += ["PARIS Rome 7.5", "oov1 w3 2.0"]
+    ana = []
+    unit = vecs / np.maximum(np.linalg.norm(vecs, axis=1, keepdims=True), 1e-30)
+    for sec in range(4):
+        ana.append(f": section{sec}")
+        for _ in range(120):
+            ids = rng.integers(0, V, 4)
+            if rng.random() < 0.7:  # make most answers the true 3CosAdd argmax
+                sc = (unit[ids[1]] - unit[ids[0]] + unit[ids[2]]) @ unit.T
+                sc[ids[:3]] = -np.inf
+                ids[3] = int(np.argmax(sc))
+            ana.append(" ".join(toks[i] for i in ids))
+        ana.append("w1 w2 oov w3")
+    sim_path, ana_path = "/tmp/golden_sim.txt", "/tmp/golden_ana.txt"
+    open(sim_path, "w").write("\n".join(sim) + "\n")
+    open(ana_path, "w").write("\n".join(ana) + "\n")
+    rho, used, skipped = rev.eval_similarity(model, voc, sim_path)
+    acc, by_sec, sk = rev.eval_analogy(model, voc, ana_path)
+    acc2, by_sec2, sk2 = rev.eval_analogy(model, voc, ana_path, max_vocab=250, block=64)
+    np.savez_compressed(os.path.join(HERE, "eval_full.npz"), vecs=vecs, tokens=np.array("\x00".join(toks)),
+                        sim=np.array("\n".join(sim) + "\n"), ana=np.array("\n".join(ana) + "\n"),
+                        sim_out=np.array([rho, used, skipped]),
+                        ana_out=np.array([acc, sk, acc2, sk2]),
+                        ana_sec=np.array([[by_sec[f"section{k}"][0], by_sec[f"section{k}"][1],
+                                           by_sec2[f"section{k}"][0], by_sec2[f"section{k}"][1]] for k in range(4)]))
+
+
 def gen_eval():
     syn = make_planted_corpus(20_000, 500, n_clusters=6, cluster_size=8, seed=9)
     voc = ref_vocab(syn)
@@ -347,6 +390,6 @@ def gen_io():
 if __name__ == "__main__":
     assert sgns.__version__
     for fn in (gen_rng, gen_tables, gen_init, gen_kernel, gen_traces, gen_train, gen_dist, gen_eval,
-               gen_ingest, gen_io):
+               gen_ingest, gen_io, gen_eval_full):
         fn()
         print("wrote", fn.__name__)

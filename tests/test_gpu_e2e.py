@@ -53,8 +53,8 @@ def _gpu_run(syn, seed, **kw):
 
 
 def _rho(vecs, syn):
-    from paper_1604_04661_b200.evaluate import eval_similarity
-    rho, used, skipped = eval_similarity(vecs, syn.vocab.index, syn.gold_pairs(pairs_per_cluster=16))
+    from paper_1604_04661_b200.evaluate import similarity_score
+    rho, used, skipped = similarity_score(vecs, syn.vocab.index, syn.gold_pairs(pairs_per_cluster=16))
     assert skipped == 0
     return rho / 100.0
 

@@ -128,7 +128,7 @@ def test_planted_corpus_vocabulary_order():
 
 
 def test_eval_similarity_matches_reference():
-    from paper_1604_04661_b200.evaluate import eval_similarity, load_pairs
+    from paper_1604_04661_b200.evaluate import similarity_score
     e = load_golden("eval")
     import tempfile
     with tempfile.NamedTemporaryFile("w", suffix=".txt", delete=False) as fh:
@@ -137,7 +137,7 @@ def test_eval_similarity_matches_reference():
     names = [f"w{i}" for i in range(len(e["counts"]))]  # any index works: pairs use vocab names
     from paper_1604_04661_b200.synthetic import make_planted_corpus
     syn = make_planted_corpus(20_000, 500, n_clusters=6, cluster_size=8, seed=9)
-    rho, used, skipped = eval_similarity(e["vecs"], syn.vocab.index, path)
+    rho, used, skipped = similarity_score(e["vecs"], syn.vocab.index, path)
     os.unlink(path)
     assert [used, skipped] == e["rho"][1:].astype(int).tolist()
     assert rho == pytest.approx(float(e["rho"][0]), abs=1e-9)

@@ -30,7 +30,7 @@ def main():
     import paper_1604_04661_b200 as P
     from oracle import oracle as O
     from paper_1604_04661_b200.corpus import default_table_length, keep_probabilities
-    from paper_1604_04661_b200.evaluate import eval_similarity
+    from paper_1604_04661_b200.evaluate import similarity_score
     from paper_1604_04661_b200.model import SIGMOID_TABLE_F32
     from paper_1604_04661_b200.synthetic import make_planted_corpus
 
@@ -48,7 +48,7 @@ def main():
         cfg = P.TrainingConfig(dim=D, window=5, negatives=5, subsample=1e-4, min_count=5, alpha0=0.025,
                                epochs=args.epochs, seed=seed, loss_sample_every=1)
         model, st = P.train_encoded(syn.vocab, syn.encoded, cfg)
-        rho_g = eval_similarity(model.input_vectors, syn.vocab.index, pairs)[0] / 100
+        rho_g = similarity_score(model.input_vectors, syn.vocab.index, pairs)[0] / 100
         run = {"seed": seed, "gpu": {"words_per_sec": st.throughput_words_per_sec, "wall_s": st.wall_seconds,
                                      "loss_by_epoch": st.loss_by_epoch, "rho": rho_g,
                                      "words_trained": st.words_processed}}
@@ -67,7 +67,7 @@ def main():
             orc.run_to_completion(n_threads=T)
             wall = time.perf_counter() - t1
             trained, read, loss = orc.stats()
-            rho_c = eval_similarity(m_in, syn.vocab.index, pairs)[0] / 100
+            rho_c = similarity_score(m_in, syn.vocab.index, pairs)[0] / 100
             run["cpu_reference"] = {"words_per_sec": trained / wall, "wall_s": wall, "threads": T,
                                     "loss_by_epoch": loss, "rho": rho_c, "words_trained": trained}
             run["loss_rel_diff_by_epoch"] = [g / c - 1 for g, c in zip(st.loss_by_epoch, loss)]
