@@ -432,7 +432,13 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
         }
       }
       __syncwarp();
-      // dC_k = sum_i (alpha err_ik) A_i, column-outer; patch u+1's prefetched copies
+      // dC_k = sum_i (alpha err_ik) A_i, column-outer; patch u+1's prefetched copies.
+      // Row base pointers (lane offset folded in) are formed once, so every scatter
+      // below addresses [row + 256 j] with an immediate offset.
+      float *orow[K1R];
+#pragma unroll
+      for (int k = 0; k < K1R; ++k)
+        orow[k] = p.mv.out_dst + off_s[m + (kk_ok(k) ? k : 0)] + 2 * lane;
 #pragma unroll
       for (int j = 0; j < NS; ++j) {
         if (!slot_ok(j)) continue;
@@ -451,7 +457,7 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
         }
 #pragma unroll
         for (int k = 0; k < K1R; ++k)
-          if (kk_ok(k)) atomicAdd(reinterpret_cast<float2 *>(p.mv.out_dst + off_s[m + k] + col), acc[k]);
+          if (kk_ok(k)) atomicAdd(reinterpret_cast<float2 *>(orow[k] + 64 * j), acc[k]);
         if (lo_bits | hi_bits) {
 #pragma unroll
           for (int k = 0; k < K1R; ++k) {
