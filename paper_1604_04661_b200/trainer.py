@@ -173,6 +173,18 @@ class DeviceCorpus:
         self.ids = ids if ids is not None else torch.from_numpy(
             np.ascontiguousarray(encoded.ids, dtype=np.int32)).to(device)
         self.offsets = offsets if offsets is not None else torch.from_numpy(self.host_offsets).to(device)
+        if self.ids.numel() < self.n_tokens:
+            raise ValueError("corpus ids shorter than its offsets")
+        if self.n_tokens:
+            lo, hi = torch.aminmax(self.ids[:self.n_tokens])
+            self.id_range = (int(lo.item()), int(hi.item()))
+        else:
+            self.id_range = (0, -1)
+
+    def check_vocab(self, vocab_size: int) -> None:
+        """The kernels do not bounds-check ids (as the reference's numba cores); refuse here."""
+        if self.id_range[0] < 0 or self.id_range[1] >= vocab_size:
+            raise ValueError(f"corpus ids span {self.id_range}, outside a vocabulary of {vocab_size}")
 
 
 class DeviceSampler:
@@ -230,6 +242,9 @@ class DeviceRun:
                  stream_base: int = 0, trace_cap: int = 0, update: bool = True):
         torch = _torch()
         self.torch = torch
+        corpus.check_vocab(model.vocab_size)
+        if sampler.vocab != model.vocab_size:
+            raise ValueError("sampler and model vocabulary sizes differ")
         self.model, self.corpus, self.sampler, self.config = model, corpus, sampler, config
         dev = model.m_in.device
         self.device = dev
