@@ -3,7 +3,7 @@
 These are the data structures the reference's training entry points accept
 (`sgns/corpus.py`), restated so a caller of the reference can hand the same
 objects to this package.  Nothing here is on the hot path: the device driver
-(`csrc/sgns_driver.cu`) consumes `EncodedCorpus.ids` / `.offsets` once they
+(`csrc/sgns_fast.cuh`, `csrc/sgns_kernels.cu`) consumes `EncodedCorpus.ids` / `.offsets` once they
 are resident in HBM, and the two samplers are built here (float64, host) and
 uploaded once per run.
 

@@ -1,18 +1,19 @@
 // sgns_device.cuh -- device building blocks of the pSGNScc hot path (sm_100a).
 //
-// One warp = one worker.  A window (one chunk of <= batch_cap inputs sharing
-// the target + K negatives) is processed by one warp:
-//   1. gather: every lane cp.async's its 16-byte column chunks of the m input
-//      rows (M_in) and k1 output rows (M_out) into the warp's shared slab
-//      (all rows land before any write: the snapshot semantics of
-//      kernel_batched.py:104-113),
-//   2. scores S = A C^T: lane-local partial dots over its columns, then a
-//      transposed butterfly leaves each lane group one finished score,
-//   3. E = alpha (label - sigma(S)) with the reference's float64 bin-index
-//      rule (model.py:108-115) or the exact sigmoid (kernel_scalar.py:30-35),
-//   4. dA_i = alpha * sum_k err_ik C_k (register C) -> red.global.add.v4.f32,
-//      dC_k = sum_i (alpha err_ik) A_i (column-outer) -> red.global.add.v4.f32
-//      (kernel_batched.py:191-210, additive row application :135-143).
+// One warp = one worker; a window (<= batch_cap inputs sharing the target + K
+// negatives) is processed by one warp.  Two window-update paths:
+//  * window_update_f2 (float32, K + 1 <= 8, d <= 512): input rows staged in shared
+//    memory by 16-byte cp.async, output rows loaded straight into registers, packed
+//    FFMA2 math on a float2 column map, a transposed butterfly reducing two inputs'
+//    scores at once, dA and dC scattered with red.global.add.v2.f32.  The production
+//    driver (sgns_fast.cuh) inlines the same math inside its software pipeline.
+//  * window_update (generic: float64, K + 1 > 8, d > 512): every row staged in shared
+//    memory, 16-byte vector math, scores reduced over 32 values.
+// Both gather every row before any write (the snapshot semantics of
+// kernel_batched.py:104-113), compute E = alpha (label - sigma(S)) with the
+// reference's float64 bin rule (model.py:108-115) or the exact sigmoid
+// (kernel_scalar.py:30-35), and apply dA = alpha sum_k err C_k and
+// dC = sum_i (alpha err) A_i additively (kernel_batched.py:135-143, :191-210).
 #pragma once
 
 #include <cstdint>
@@ -211,11 +212,11 @@ __device__ __forceinline__ void cell_error_f32(float s, int k, float alpha, cons
 }
 
 // ------------------------------------------------------ window update ----
-// ids_s: m input ids then k1 output ids (target first).  rows_s: (m + k1) rows
-// of ld elements.  e_s: m * k1 scaled errors (+ m * k1 raw errors in the
-// shared-C variant).  CREG: C lives in registers (k1 <= K1R); otherwise it is
-// read from shared memory and k1 <= 32.
-template <typename T, int NCH, bool CREG, int K1R>
+// Generic path (float64, K + 1 > 8, d > 512, or V * ld >= 2^32): every row of the
+// window is staged in shared memory and read back from there.  ids_s: m input ids then
+// k1 output ids (target first).  rows_s: (m + k1) rows of ld elements.  e_s: m * k1
+// scaled errors followed by m * k1 raw errors.  k1 <= 32.
+template <typename T, int NCH>
 __device__ __forceinline__ void window_update(const ModelView<T> &mv, const int *ids_s, int m,
                                               int k1, T alpha, bool exact, const T *sig_s,
                                               bool want_loss, double &loss_acc,
@@ -227,7 +228,7 @@ __device__ __forceinline__ void window_update(const ModelView<T> &mv, const int 
   const int nvec = mv.nvec;
   const int nrows = m + k1;
 
-  // 1. gather every row of the window before any scatter (snapshot semantics)
+  // gather every row of the window before any scatter (snapshot semantics)
   for (int r = 0; r < nrows; ++r) {
     const int id = ids_s[r];
     const T *src = (r < m ? mv.in_src : mv.out_src) + (int64_t)id * ld;
@@ -240,94 +241,7 @@ __device__ __forceinline__ void window_update(const ModelView<T> &mv, const int 
   }
   cp_async_wait_all();
   // each lane reads back only the chunks it copied itself: no warp barrier needed
-
-  if constexpr (CREG) {
-    constexpr int NV = (K1R <= 8) ? 8 : 16;
-    V c[K1R][NCH];
-#pragma unroll
-    for (int k = 0; k < K1R; ++k)
-#pragma unroll
-      for (int j = 0; j < NCH; ++j) {
-        const int ch = lane + 32 * j;
-        c[k][j] = (k < k1 && ch < nvec)
-                      ? *reinterpret_cast<const V *>(rows_s + (int64_t)(m + k) * ld + ch * VN)
-                      : vzero(T());
-      }
-    const int my_k = reduced_index<NV>(lane);
-    const bool leader = (lane & ((32 / NV) - 1)) == 0;
-    for (int i = 0; i < m; ++i) {
-      V a[NCH];
-#pragma unroll
-      for (int j = 0; j < NCH; ++j) {
-        const int ch = lane + 32 * j;
-        a[j] = ch < nvec ? *reinterpret_cast<const V *>(rows_s + (int64_t)i * ld + ch * VN)
-                         : vzero(T());
-      }
-      T p[NV];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        T acc = T(0);
-        if (k < K1R) {
-#pragma unroll
-          for (int j = 0; j < NCH; ++j) acc += vdot(a[j], c[k < K1R ? k : 0][j]);
-        }
-        p[k] = acc;
-      }
-      const T s = transpose_reduce<NV>(p, lane);
-      T er = T(0), es = T(0);
-      if (my_k < k1) {
-        cell_error<T>(s, my_k, alpha, exact, sig_s, er, es);
-        if (leader) {
-          e_s[i * k1 + my_k] = es;
-          if (want_loss) {
-            loss_acc += softplus(my_k == 0 ? -(double)s : (double)s);
-            cell_acc += 1;
-          }
-        }
-      }
-      // dA_i = alpha * sum_k err_ik C_k  (alpha applied after the sum, :201-210)
-      V d[NCH];
-#pragma unroll
-      for (int j = 0; j < NCH; ++j) d[j] = vzero(T());
-#pragma unroll
-      for (int k = 0; k < K1R; ++k) {
-        const T ek = __shfl_sync(0xffffffffu, er, group_leader<NV>(k));
-        if (k < k1) {
-#pragma unroll
-          for (int j = 0; j < NCH; ++j) vfma(d[j], ek, c[k][j]);
-        }
-      }
-      T *dst = mv.in_dst + (int64_t)ids_s[i] * ld;
-#pragma unroll
-      for (int j = 0; j < NCH; ++j) {
-        const int ch = lane + 32 * j;
-        if (ch < nvec) {
-          vscale(d[j], alpha);
-          red_add(dst + ch * VN, d[j]);
-        }
-      }
-    }
-    __syncwarp();
-    // dC_k = sum_i (alpha err_ik) A_i, one column chunk at a time
-#pragma unroll
-    for (int j = 0; j < NCH; ++j) {
-      const int ch = lane + 32 * j;
-      V acc[K1R];
-#pragma unroll
-      for (int k = 0; k < K1R; ++k) acc[k] = vzero(T());
-      if (ch < nvec) {
-        for (int i = 0; i < m; ++i) {
-          const V a = *reinterpret_cast<const V *>(rows_s + (int64_t)i * ld + ch * VN);
-#pragma unroll
-          for (int k = 0; k < K1R; ++k)
-            if (k < k1) vfma(acc[k], e_s[i * k1 + k], a);
-        }
-#pragma unroll
-        for (int k = 0; k < K1R; ++k)
-          if (k < k1) red_add(mv.out_dst + (int64_t)ids_s[m + k] * ld + ch * VN, acc[k]);
-      }
-    }
-  } else {
+  {
     // shared-memory C (k1 <= 32): scores, errors to smem, then dA and dC passes
     constexpr int NV = 32;
     T *er_s = e_s + m * k1;

@@ -83,7 +83,7 @@ __device__ __forceinline__ void run_window(const ModelView<T> &mv, const int *id
     window_update_f2<NS, NCH, K1R, K1R == 6>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss,
                                              cells, rows_s, e_s, lane);
   } else {
-    window_update<T, NCH, false, 0>(mv, ids_s, m, k1, alpha, exact, sig_s, want, loss, cells,
+    window_update<T, NCH>(mv, ids_s, m, k1, alpha, exact, sig_s, want, loss, cells,
                                     rows_s, e_s, lane);
   }
 }
