@@ -319,7 +319,9 @@ def main():
     V = len(counts)
     # configs[3] is one epoch; if --steps asks for more words than the shard holds, the
     # workers wrap into further epochs so every timed step does a full period of work
-    shard_tokens = int(enc.offsets[shard[1]] - enc.offsets[shard[0]])
+    # identical on every rank: sized by the smallest shard
+    from paper_1604_04661_b200.corpus import partition_sentences
+    shard_tokens = min(int(enc.offsets[b] - enc.offsets[a]) for a, b in partition_sentences(enc, world))
     epochs = max(1, math.ceil((args.warmup + args.steps + 1) * args.period / max(shard_tokens, 1)))
     cfg = TrainingConfig(dim=DIM, window=WINDOW, negatives=NEG, subsample=SUBSAMPLE, min_count=5,
                          alpha0=ALPHA0, epochs=epochs, seed=args.seed, rng="philox")
