@@ -477,13 +477,16 @@ def e2e_leg(args, corpus, enc, shard, cfg, counts, keep, world, rank, dev, alpha
                           alpha0_eff=alpha0_eff, keep_probs=keep)
     stream = torch.cuda.current_stream(dev)
 
-    def chunk(i):
-        a, b = bounds[i], bounds[i + 1]
-        base = int(off[a])
-        return st.train_chunk(host_ids[base - tok_lo:int(off[b]) - tok_lo], off[a:b + 1] - base, base)
+    off_pinned = torch.from_numpy(np.ascontiguousarray(off, dtype=np.int64)).pin_memory()
 
-    for i in range(args.warmup):
-        chunk(i)
+    def chunks(lo, hi):
+        for i in range(lo, hi):
+            a, b = bounds[i], bounds[i + 1]
+            base = int(off[a])
+            yield (host_ids[base - tok_lo:int(off[b]) - tok_lo], off_pinned[a:b + 1] - base, base)
+
+    for _ in st.train_chunks(chunks(0, args.warmup)):
+        pass
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -492,8 +495,7 @@ def e2e_leg(args, corpus, enc, shard, cfg, counts, keep, world, rank, dev, alpha
     wall0 = time.perf_counter()
     trained = 0
     h2d = d2h = 0
-    for i in range(args.warmup, n_chunks):
-        tr, rd, ls, cl, inp, ch = chunk(i)
+    for tr, rd, ls, cl, inp, ch in st.train_chunks(chunks(args.warmup, n_chunks)):
         trained += tr
         h2d += st.h2d_bytes
         d2h += st.d2h_bytes
@@ -512,7 +514,8 @@ def e2e_leg(args, corpus, enc, shard, cfg, counts, keep, world, rank, dev, alpha
     torch.cuda.empty_cache()
     return {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
             "d2h_bytes_per_step": d2h // args.steps, "wall_seconds": wall,
-            "api": "StreamingTrainer.train_chunk (pinned host chunk -> sgns_drive -> counters)"}
+            "api": "StreamingTrainer.train_chunks: pinned host chunk -> H2D (side stream, overlapped "
+                   "with the previous chunk) -> sgns_drive -> 64-byte counters D2H, every step"}
 
 
 if __name__ == "__main__":

@@ -120,6 +120,11 @@ typedef struct sgns_drive_params {
   int64_t claim_end;
   int64_t shard_lo, shard_hi;
   int64_t words_base;
+  /* optional (dynamic schedule): per-launch totals accumulated by the workers at exit,
+   * int64[6] = {words_trained, words_read, chunks, inputs, loss_cells, (unused)} and
+   * double[1] = {loss_sum}; the caller zeroes them before the launch. */
+  int64_t *d_totals;
+  double *d_loss_total;
 } sgns_drive_params;
 
 enum { SGNS_SCHEDULE_STATIC = 0, SGNS_SCHEDULE_DYNAMIC = 1 };

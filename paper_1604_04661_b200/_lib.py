@@ -43,7 +43,7 @@ class DriveParams(C.Structure):
         ("d_trace", P), ("d_trace_alpha", P), ("d_trace_count", P), ("d_error", P),
         ("warps_per_block", I32), ("token_base", I64), ("epoch_base", I32),
         ("schedule", I32), ("d_claim", P), ("claim_end", I64), ("shard_lo", I64),
-        ("shard_hi", I64), ("words_base", I64),
+        ("shard_hi", I64), ("words_base", I64), ("d_totals", P), ("d_loss_total", P),
     ]
 
 

@@ -53,6 +53,8 @@ struct FastArgs {
   int64_t token_base;
   uint32_t epoch_base;
   int64_t words_base;
+  unsigned long long *totals;  // optional, see sgns_drive_params.d_totals
+  double *loss_total;
 };
 
 struct FastSlab {
@@ -487,6 +489,16 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
     if (lane == 0) {
       p.loss_by_epoch[(int64_t)wid * p.epochs + loss_epoch] += loss;
       p.cells_by_epoch[(int64_t)wid * p.epochs + loss_epoch] += cells;
+    }
+  }
+  if (lane == 0 && p.totals != nullptr) {
+    atomicAdd(p.totals + 0, (unsigned long long)trained);
+    atomicAdd(p.totals + 1, (unsigned long long)read);
+    atomicAdd(p.totals + 2, (unsigned long long)chunks);
+    atomicAdd(p.totals + 3, (unsigned long long)inputs);
+    if (loss_epoch >= 0) {
+      atomicAdd(p.totals + 4, (unsigned long long)cells);
+      atomicAdd(p.loss_total, loss);
     }
   }
   if (lane == 0) {

@@ -756,6 +756,8 @@ static int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resid
   a.token_base = p->token_base;
   a.epoch_base = (uint32_t)p->epoch_base;
   a.words_base = p->words_base;
+  a.totals = reinterpret_cast<unsigned long long *>(p->d_totals);
+  a.loss_total = p->d_loss_total;
   const int wpb = p->warps_per_block;
   switch (ns_for(p->ld)) {
     case 1: return fast_ns<1>(a, wpb, st, resident);

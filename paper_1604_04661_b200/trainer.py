@@ -495,13 +495,13 @@ def train(corpus_path: str, config: TrainingConfig, progress: bool = False):
 
 
 class StreamingTrainer:
-    """Out-of-core training: sentence chunks stream from (pinned) host memory
-    through preallocated HBM buffers while the model, sampler and alpha
-    schedule stay resident.  Each `train_chunk` is one host->device copy, one
-    driver launch over the chunk (dynamic schedule: workers claim its
-    sentences), and one small device->host read of the chunk's counters.
-    Draws are keyed by the global corpus position (`token_base`) and alpha by
-    the global words-read position, so chunking does not change the training."""
+    """Out-of-core training: sentence chunks stream from pinned host memory through
+    two preallocated HBM buffer sets while the model, sampler and alpha schedule stay
+    resident.  `train_chunks` pipelines: chunk i+1's host->device copy runs on a side
+    stream while chunk i trains, and chunk i's counters (accumulated by the kernel into
+    a 64-byte totals block) are read back once chunk i+1 is launched.  Draws are keyed
+    by the global corpus position (`token_base`) and alpha by the global words-read
+    position, so chunking does not change the training."""
 
     def __init__(self, model: DeviceModel, counts: np.ndarray, config: TrainingConfig,
                  total_x_epochs: float, max_chunk_tokens: int, max_chunk_sentences: int,
@@ -516,8 +516,17 @@ class StreamingTrainer:
         self.model, self.config = model, config
         dev = model.m_in.device
         self.device = dev
-        self.ids = torch.empty(max_chunk_tokens, dtype=torch.int32, device=dev)
-        self.offsets = torch.empty(max_chunk_sentences + 1, dtype=torch.int64, device=dev)
+        self.max_tok, self.max_sent = max_chunk_tokens, max_chunk_sentences
+        self.ids = [torch.empty(max_chunk_tokens, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.offsets = [torch.empty(max_chunk_sentences + 1, dtype=torch.int64, device=dev) for _ in range(2)]
+        self.off_pinned = [torch.empty(max_chunk_sentences + 1, dtype=torch.int64).pin_memory()
+                           for _ in range(2)]
+        self.acc = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in range(2)]  # totals + loss
+        self.acc_host = [torch.zeros(8, dtype=torch.int64).pin_memory() for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream(dev)
+        self.copied = [torch.cuda.Event() for _ in range(2)]
+        self.trained_ev = [torch.cuda.Event() for _ in range(2)]
+        self.read_ev = [torch.cuda.Event() for _ in range(2)]
         self.sampler = DeviceSampler(counts, "philox", device=dev)
         if keep_probs is None and config.subsample > 0:
             from .corpus import keep_probabilities
@@ -534,14 +543,11 @@ class StreamingTrainer:
         self.loss = torch.zeros((n_workers, 1), dtype=torch.float64, device=dev)
         self.cells = torch.zeros((n_workers, 1), dtype=torch.int64, device=dev)
         self.shared = torch.zeros(2, dtype=torch.int64, device=dev)
-        self.stats_dev = torch.zeros(6, dtype=torch.float64, device=dev)
-        self.stats_host = torch.zeros(6, dtype=torch.float64).pin_memory()
         self.sig = device_sigmoid_table(model.np_dtype, dev)
         p = _lib.DriveParams()
         p.dtype = model.cdtype
         p.d_m_in, p.d_m_out = model.m_in.data_ptr(), model.m_out.data_ptr()
         p.vocab, p.ld, p.dim = model.vocab_size, model.ld, model.dim
-        p.d_ids, p.d_offsets = self.ids.data_ptr(), self.offsets.data_ptr()
         p.d_keep_probs = None if self.keep is None else self.keep.data_ptr()
         p.rng_mode = _lib.RNG_PHILOX
         p.d_alias_thr, p.d_alias_idx = self.sampler.alias_thr.data_ptr(), self.sampler.alias_idx.data_ptr()
@@ -567,45 +573,87 @@ class StreamingTrainer:
         self.h2d_bytes = 0
         self.d2h_bytes = 0
 
-    def train_chunk(self, ids_host, offsets_host: np.ndarray, token_base: int, epoch: int = 0,
-                    words_base: int | None = None):
-        """Train one chunk.  ids_host: pinned torch int32 tensor of its tokens;
-        offsets_host: its int64 sentence offsets starting at 0; token_base: corpus
-        position of its first token; words_base: words read before it (default
-        token_base).  Returns (words_trained, words_read, loss_sum, loss_cells,
-        inputs, chunks) of the chunk."""
+    def _stage(self, buf: int, ids_host, offsets_host) -> tuple[int, int]:
+        """Queue the host->device copies of one chunk into buffer set `buf` (side stream)."""
         torch = self.torch
-        n_tok = int(offsets_host[-1])
         n_sent = len(offsets_host) - 1
-        if n_sent < 1:
-            return 0, 0, 0.0, 0, 0, 0
-        if n_tok > self.ids.numel() or n_sent + 1 > self.offsets.numel():
+        n_tok = int(offsets_host[-1])
+        if n_tok > self.max_tok or n_sent > self.max_sent:
             raise ValueError("chunk larger than the streaming buffers")
-        self.ids[:n_tok].copy_(ids_host[:n_tok], non_blocking=True)
-        off_t = torch.from_numpy(np.ascontiguousarray(offsets_host, dtype=np.int64))
-        self.offsets[:n_sent + 1].copy_(off_t)
-        self.workers.zero_()
-        self.loss.zero_()
-        self.cells.zero_()
-        self.claim.zero_()
+        if torch.is_tensor(offsets_host) and offsets_host.is_pinned():
+            off_src = offsets_host
+        else:
+            self.copied[buf].synchronize()  # the staging buffer's previous copy has landed
+            self.off_pinned[buf][:n_sent + 1].copy_(torch.as_tensor(np.asarray(offsets_host, dtype=np.int64)))
+            off_src = self.off_pinned[buf][:n_sent + 1]
+        with torch.cuda.stream(self.copy_stream):
+            self.copy_stream.wait_event(self.trained_ev[buf])  # previous user of this buffer set
+            self.ids[buf][:n_tok].copy_(ids_host[:n_tok], non_blocking=True)
+            self.offsets[buf][:n_sent + 1].copy_(off_src, non_blocking=True)
+            self.copied[buf].record(self.copy_stream)
+        return n_tok, n_sent
+
+    def _launch(self, buf: int, n_tok: int, n_sent: int, token_base: int, epoch: int, words_base: int):
+        torch = self.torch
+        stream = torch.cuda.current_stream(self.device)
+        stream.wait_event(self.copied[buf])
+        self.acc[buf].zero_()
         p = self.params
+        p.d_ids, p.d_offsets = self.ids[buf].data_ptr(), self.offsets[buf].data_ptr()
         p.shard_hi = n_sent
         p.claim_end = n_sent
         p.token_base = int(token_base)
         p.epoch_base = int(epoch)
-        p.words_base = int(token_base if words_base is None else words_base)
-        _lib.check(_lib.lib().sgns_drive(p, current_stream_ptr(self.device)), "sgns_drive")
-        wv = self.workers.view(torch.int64).view(self.n_workers, WORKER_DTYPE.itemsize // 8)
-        # int64 columns of sgns_worker: 8 kernel_counter, 10 words_trained, 11 inputs
-        self.stats_dev[0] = wv[:, 10].sum().double()
-        self.stats_dev[1] = float(n_tok)
-        self.stats_dev[2] = self.loss.sum()
-        self.stats_dev[3] = self.cells.sum().double()
-        self.stats_dev[4] = wv[:, 11].sum().double()
-        self.stats_dev[5] = wv[:, 8].sum().double()
-        self.stats_host.copy_(self.stats_dev, non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize()
-        s = self.stats_host.numpy()
+        p.words_base = int(words_base)
+        p.d_totals = self.acc[buf].data_ptr()
+        p.d_loss_total = self.acc[buf][6:7].data_ptr()
+        self.claim.zero_()
+        _lib.check(_lib.lib().sgns_drive(p, stream.cuda_stream), "sgns_drive")
+        self.trained_ev[buf].record(stream)
+        self.acc_host[buf].copy_(self.acc[buf], non_blocking=True)
+        self.read_ev[buf].record(stream)
         self.h2d_bytes = n_tok * 4 + (n_sent + 1) * 8
-        self.d2h_bytes = self.stats_host.numel() * 8
-        return int(s[0]), int(s[1]), float(s[2]), int(s[3]), int(s[4]), int(s[5])
+        self.d2h_bytes = self.acc_host[buf].numel() * 8
+
+    def _result(self, buf: int):
+        self.read_ev[buf].synchronize()
+        a = self.acc_host[buf].numpy()
+        loss = float(a[6:7].view(np.float64)[0])
+        # (words_trained, words_read, loss_sum, loss_cells, inputs, chunks)
+        return int(a[0]), int(a[1]), loss, int(a[4]), int(a[3]), int(a[2])
+
+    def train_chunks(self, chunks):
+        """Train an iterable of (ids_host, offsets_host, token_base[, epoch[, words_base]])
+        chunks with copy/compute overlap; yields each chunk's counters in order."""
+        it = iter(chunks)
+        try:
+            nxt = next(it)
+        except StopIteration:
+            return
+        buf = 0
+        staged = self._stage(buf, nxt[0], nxt[1])
+        pending = None
+        while nxt is not None:
+            cur, cur_buf, cur_staged = nxt, buf, staged
+            try:
+                nxt = next(it)
+            except StopIteration:
+                nxt = None
+            if cur_staged[1] > 0:
+                epoch = cur[3] if len(cur) > 3 else 0
+                words_base = cur[4] if len(cur) > 4 else cur[2]
+                self._launch(cur_buf, cur_staged[0], cur_staged[1], cur[2], epoch, words_base)
+            if nxt is not None:
+                buf ^= 1
+                staged = self._stage(buf, nxt[0], nxt[1])
+            if pending is not None:
+                yield self._result(pending) if pending >= 0 else (0, 0, 0.0, 0, 0, 0)
+            pending = cur_buf if cur_staged[1] > 0 else -1
+        if pending is not None:
+            yield self._result(pending) if pending >= 0 else (0, 0, 0.0, 0, 0, 0)
+
+    def train_chunk(self, ids_host, offsets_host, token_base: int, epoch: int = 0,
+                    words_base: int | None = None):
+        """One chunk, synchronously (see train_chunks for the pipelined form)."""
+        wb = token_base if words_base is None else words_base
+        return next(iter(self.train_chunks([(ids_host, offsets_host, token_base, epoch, wb)])))

@@ -391,3 +391,34 @@ def test_fast_driver_single_worker_trains_like_oracle():
     np.testing.assert_allclose(run.loss_by_epoch(), orc.stats()[2], rtol=1e-3)
     assert np.abs(got.input_vectors - m_in).max() < 1e-3 * np.abs(m_in).max()
     assert np.abs(got.output_vectors - m_out).max() < 1e-3 * np.abs(m_out).max()
+
+
+def test_streaming_chunks_equal_resident_training():
+    """StreamingTrainer.train_chunks (double-buffered, one worker) trains exactly what the
+    resident dynamic-schedule run trains on the same corpus: same windows -> same model."""
+    P = _pkg()
+    from paper_1604_04661_b200.synthetic import make_planted_corpus
+    from paper_1604_04661_b200.model import DeviceModel
+    from paper_1604_04661_b200.trainer import StreamingTrainer
+    syn = make_planted_corpus(40_000, 500, n_clusters=4, cluster_size=5, sentence_len=37, seed=8)
+    ids, off, counts = syn.encoded.ids, syn.encoded.offsets, syn.vocab.counts
+    V, D = len(counts), 64
+    base = np.random.default_rng(1).normal(size=(V, D)).astype(np.float32) * 0.1
+    dm1 = DeviceModel.from_host(P.EmbeddingModel(base.copy(), np.zeros_like(base)))
+    run, _ = _run_driver(ids, off, counts, window=5, k=5, cap=16, dynamic=True, subsample=1e-3,
+                         seed=9, stream_base=0, table_len=None, rng="philox", workers=1, epochs=1,
+                         update=True, model=dm1, dim=D, trace_cap=0, schedule="dynamic")
+    dm2 = DeviceModel.from_host(P.EmbeddingModel(base.copy(), np.zeros_like(base)))
+    cfg = P.TrainingConfig(dim=D, window=5, negatives=5, subsample=1e-3, min_count=1, seed=9,
+                           epochs=1, workers=1)
+    st = StreamingTrainer(dm2, counts, cfg, float(off[-1]), 20_000, 2_000, syn.encoded.max_sentence_length(),
+                          n_workers=1)
+    cuts = [0, 100, 333, 334, 700, len(off) - 1]
+    host_ids = torch.from_numpy(ids).pin_memory()
+    chunks = [(host_ids[off[a]:off[b]], off[a:b + 1] - off[a], int(off[a])) for a, b in zip(cuts, cuts[1:])]
+    res = list(st.train_chunks(chunks))
+    assert sum(r[1] for r in res) == int(off[-1])
+    assert sum(r[0] for r in res) == run.words_trained
+    a, b = dm1.to_host(), dm2.to_host()
+    np.testing.assert_allclose(b.input_vectors, a.input_vectors, rtol=0, atol=1e-6)
+    np.testing.assert_allclose(b.output_vectors, a.output_vectors, rtol=0, atol=1e-6)
