@@ -453,4 +453,123 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
   __syncwarp();
 }
 
+
+// float32, 8 < k1 <= 16, d <= 512: like window_update_f2 but the k1 output rows stay in
+// shared memory (16 x NS float2 would not fit in registers).  Each C-row slot load is
+// shared by a pair of inputs; one transposed butterfly over 32 values reduces both
+// inputs' scores; error rows are padded to 16 floats.  rows_s holds the m input rows
+// then the k1 output rows.
+template <int NS, int NCH>
+__device__ __forceinline__ void window_update_f2s(const ModelView<float> &mv, const uint32_t *off_s,
+                                                  int m, int k1, float alpha, bool exact,
+                                                  const float *sig_s, bool want_loss,
+                                                  double &loss_acc, long long &cell_acc,
+                                                  float *rows_s, float *e_s, int lane) {
+  constexpr int KM = 16;
+  const int64_t ld = mv.ld;
+  const int nvec = mv.nvec, nslot = nvec * 2;
+  auto slot_ok = [&](int j) { return j < NS - 1 || lane + 32 * j < nslot; };
+  auto chunk_ok = [&](int j) { return j < NCH - 1 || lane + 32 * j < nvec; };
+  for (int r = 0; r < m + k1; ++r) {
+    const float *src = (r < m ? mv.in_src : mv.out_src) + off_s[r];
+    float *dst = rows_s + (int64_t)r * ld;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j)
+      if (chunk_ok(j)) cp_async16(dst + (lane + 32 * j) * 4, src + (lane + 32 * j) * 4);
+  }
+  cp_async_wait_all();
+  __syncwarp();
+  const float *c_s = rows_s + (int64_t)m * ld;
+  float *er_s = e_s + m * KM;  // raw errors after the scaled ones
+  const float2 alpha2 = make_float2(alpha, alpha);
+  for (int i = 0; i < m; i += 2) {
+    const bool two = i + 1 < m;
+    const int i1 = two ? i + 1 : i;
+    float2 a0[NS], a1[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const int col = 2 * (lane + 32 * j);
+      a0[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col) : f2zero();
+      a1[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)i1 * ld + col) : f2zero();
+    }
+    float pp[2 * KM];
+#pragma unroll
+    for (int k = 0; k < KM; ++k) {
+      float2 s0 = f2zero(), s1 = f2zero();
+      if (k < k1) {
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+          const float2 c = slot_ok(j) ? *reinterpret_cast<const float2 *>(c_s + (int64_t)k * ld + 2 * (lane + 32 * j))
+                                      : f2zero();
+          s0 = __ffma2_rn(a0[j], c, s0);
+          s1 = __ffma2_rn(a1[j], c, s1);
+        }
+      }
+      pp[k] = s0.x + s0.y;
+      pp[KM + k] = s1.x + s1.y;
+    }
+    const float sc = transpose_reduce<2 * KM>(pp, lane);  // value v = h * 16 + k on lane v
+    const int hk = lane >> 4, kk = lane & 15;
+    const bool live = kk < k1 && (hk == 0 || two);
+    float er = 0.f, es = 0.f;
+    if (live) {
+      if (exact) cell_error<float>(sc, kk, alpha, true, sig_s, er, es);
+      else cell_error_f32(sc, kk, alpha, sig_s, er, es);
+      e_s[(i + hk) * KM + kk] = es;
+      er_s[(i + hk) * KM + kk] = er;
+      if (want_loss) {
+        loss_acc += softplus(kk == 0 ? -(double)sc : (double)sc);
+        cell_acc += 1;
+      }
+    }
+    __syncwarp();
+    // dA for both inputs, each C slot loaded once
+    float2 d0[NS], d1[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) d0[j] = d1[j] = f2zero();
+    for (int k = 0; k < k1; ++k) {
+      const float e0 = er_s[i * KM + k], e1 = er_s[i1 * KM + k];
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+        const float2 c = slot_ok(j) ? *reinterpret_cast<const float2 *>(c_s + (int64_t)k * ld + 2 * (lane + 32 * j))
+                                    : f2zero();
+        d0[j] = __ffma2_rn(make_float2(e0, e0), c, d0[j]);
+        d1[j] = __ffma2_rn(make_float2(e1, e1), c, d1[j]);
+      }
+    }
+    float *dst0 = mv.in_dst + off_s[i] + 2 * lane;
+    float *dst1 = mv.in_dst + off_s[i1] + 2 * lane;
+#pragma unroll
+    for (int j = 0; j < NS; ++j)
+      if (slot_ok(j)) {
+        atomicAdd(reinterpret_cast<float2 *>(dst0 + 64 * j), __fmul2_rn(d0[j], alpha2));
+        if (two) atomicAdd(reinterpret_cast<float2 *>(dst1 + 64 * j), __fmul2_rn(d1[j], alpha2));
+      }
+  }
+  __syncwarp();
+  // dC_k = sum_i (alpha err_ik) A_i, column-outer, outputs in groups of 8
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+    if (!slot_ok(j)) continue;
+    const int col = 2 * (lane + 32 * j);
+    for (int k0 = 0; k0 < k1; k0 += 8) {
+      float2 acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = f2zero();
+      for (int i = 0; i < m; ++i) {
+        const float2 a = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col);
+        const float4 e03 = *reinterpret_cast<const float4 *>(e_s + i * KM + k0);
+        const float4 e47 = *reinterpret_cast<const float4 *>(e_s + i * KM + k0 + 4);
+        const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = __ffma2_rn(make_float2(ev[q], ev[q]), a, acc[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (k0 + q < k1) atomicAdd(reinterpret_cast<float2 *>(mv.out_dst + off_s[m + k0 + q] + col), acc[q]);
+    }
+  }
+  __syncwarp();
+}
+
 }  // namespace sgns

@@ -30,13 +30,14 @@ struct Slab {
   int64_t rows, e, ids, roff, kept, off, total;
 };
 // MODE_F2: float32 fast path (only the m input rows are staged); MODE_SMEM: all rows staged
-enum { MODE_SMEM = 0, MODE_F2 = 1 };
+enum { MODE_SMEM = 0, MODE_F2 = 1, MODE_F2S = 2 };
 __host__ __device__ inline Slab slab_layout(int mode, int64_t elem, int64_t ld, int mcap, int k1,
                                             int kept_cap) {
   Slab s;
   s.rows = 0;
   s.e = round16((int64_t)(mode == MODE_F2 ? mcap : mcap + k1) * ld * elem);
-  s.ids = s.e + round16((int64_t)2 * mcap * (k1 > 8 ? k1 : 8) * elem);  // F2 rows padded to 8
+  const int erow = mode == MODE_F2S ? 16 : (k1 > 8 ? k1 : 8);  // F2 error rows padded to 8 / 16
+  s.ids = s.e + round16((int64_t)2 * mcap * erow * elem);
   s.roff = s.ids + round16((int64_t)(mcap + k1) * 4);
   s.kept = s.roff + round16((int64_t)(mcap + k1) * 4);
   s.off = s.kept + round16((int64_t)kept_cap * 4);
@@ -82,6 +83,11 @@ __device__ __forceinline__ void run_window(const ModelView<T> &mv, const int *id
     __syncwarp();
     window_update_f2<NS, NCH, K1R, K1R == 6>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss,
                                              cells, rows_s, e_s, lane);
+  } else if constexpr (MODE == MODE_F2S) {
+    for (int r = lane; r < m + k1; r += 32) roff_s[r] = (uint32_t)ids_s[r] * (uint32_t)mv.ld;
+    __syncwarp();
+    window_update_f2s<NS, NCH>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss, cells, rows_s,
+                               e_s, lane);
   } else {
     window_update<T, NCH>(mv, ids_s, m, k1, alpha, exact, sig_s, want, loss, cells,
                                     rows_s, e_s, lane);
@@ -103,7 +109,7 @@ template <typename T> struct UpdateArgs {
 };
 
 template <typename T, int MODE, int NS, int NCH, int K1R>
-__global__ void __launch_bounds__(256, MODE == MODE_F2 ? 2 : 1) update_windows_kernel(UpdateArgs<T> p) {
+__global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) update_windows_kernel(UpdateArgs<T> p) {
   extern __shared__ __align__(16) unsigned char smem[];
   T *sig_s = reinterpret_cast<T *>(smem);
   load_table(sig_s, p.sig);
@@ -182,7 +188,7 @@ struct SmBatch {
 };
 
 template <typename T, int MODE, int NS, int NCH, int K1R, int RNG>
-__global__ void __launch_bounds__(256, MODE == MODE_F2 ? 2 : 1) drive_kernel(DriveArgs<T> p) {
+__global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) drive_kernel(DriveArgs<T> p) {
   extern __shared__ __align__(16) unsigned char smem[];
   T *sig_s = reinterpret_cast<T *>(smem);
   load_table(sig_s, p.sig);
@@ -554,9 +560,26 @@ static int drive_f2(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
   return launch_drive_t<float, MODE_F2, NS, NCH, 8, RNG>(a, wpb, st, res);
 }
 
+template <int NS, int RNG>
+static int drive_f2s(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
+  return launch_drive_t<float, MODE_F2S, NS, (NS + 1) / 2, 16, RNG>(a, wpb, st, res);
+}
+
 template <int RNG>
 static int drive_f32(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
   const int ns = ns_for(a.mv.ld);
+  if (a.k_neg + 1 > 8 && a.k_neg + 1 <= 16 && offsets32_ok(a.vocab, a.mv.ld)) {
+    switch (ns) {
+      case 1: return drive_f2s<1, RNG>(a, wpb, st, res);
+      case 2: return drive_f2s<2, RNG>(a, wpb, st, res);
+      case 3: return drive_f2s<3, RNG>(a, wpb, st, res);
+      case 4: return drive_f2s<4, RNG>(a, wpb, st, res);
+      case 5: return drive_f2s<5, RNG>(a, wpb, st, res);
+      case 6: return drive_f2s<6, RNG>(a, wpb, st, res);
+      case 7: return drive_f2s<7, RNG>(a, wpb, st, res);
+      case 8: return drive_f2s<8, RNG>(a, wpb, st, res);
+    }
+  }
   if (a.k_neg + 1 <= 8 && offsets32_ok(a.vocab, a.mv.ld)) {
     switch (ns) {
       case 1: return drive_f2<1, RNG>(a, wpb, st, res);
@@ -598,8 +621,25 @@ static int update_f2(UpdateArgs<float> a, cudaStream_t st) {
   return launch_update_t<float, MODE_F2, NS, NCH, 8>(a, st);
 }
 
+template <int NS>
+static int update_f2s(UpdateArgs<float> a, cudaStream_t st) {
+  return launch_update_t<float, MODE_F2S, NS, (NS + 1) / 2, 16>(a, st);
+}
+
 static int update_f32(UpdateArgs<float> a, cudaStream_t st) {
   const int ns = ns_for(a.mv.ld);
+  if (a.k1 > 8 && a.k1 <= 16 && offsets32_ok(a.vocab, a.mv.ld)) {
+    switch (ns) {
+      case 1: return update_f2s<1>(a, st);
+      case 2: return update_f2s<2>(a, st);
+      case 3: return update_f2s<3>(a, st);
+      case 4: return update_f2s<4>(a, st);
+      case 5: return update_f2s<5>(a, st);
+      case 6: return update_f2s<6>(a, st);
+      case 7: return update_f2s<7>(a, st);
+      case 8: return update_f2s<8>(a, st);
+    }
+  }
   if (a.k1 <= 8 && offsets32_ok(a.vocab, a.mv.ld)) {
     switch (ns) {
       case 1: return update_f2<1>(a, st);

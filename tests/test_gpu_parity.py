@@ -136,7 +136,9 @@ def _random_windows(rng, V, n, m_max, k, disjoint=False):
 
 
 @pytest.mark.parametrize("dtype,D,k", [("f64", 300, 5), ("f32", 300, 5), ("f32", 100, 5),
-                                       ("f32", 200, 10), ("f32", 300, 15), ("f64", 24, 3)])
+                                       ("f32", 200, 10), ("f32", 300, 15), ("f32", 512, 15),
+                                       ("f32", 64, 8), ("f32", 40, 12), ("f32", 300, 16),
+                                       ("f64", 24, 3)])
 def test_disjoint_windows_equal_sequential(dtype, D, k):
     """P2: a batch of row-disjoint windows == the sequential oracle application."""
     P, O = _pkg(), _oracle()
