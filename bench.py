@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--workers", type=int, default=0, help="device workers (0: resident warps)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--micro-ids", choices=["zipf", "uniform"], default="zipf",
+                    help="--config micro: id distribution (uniform = no hot rows, diagnostic)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--sync-hot-rows", type=int, default=-1,
@@ -219,14 +221,37 @@ def config_block(args, world):
             "l2": "model 2.4 GB and corpus 3.2 GB exceed the 126 MB L2; no flush between steps"}
 
 
+def micro_cpu_leg(base_in, base_out, off, ins, outs, wbytes, wflops, T):
+    """The same windows through the oracle's restatement of the reference core on host
+    threads (test infrastructure as the checker-side baseline; kind "port")."""
+    from oracle import oracle as O
+    from paper_1604_04661_b200.model import SIGMOID_TABLE_F32
+    out = {"kind": "port", "cores_available": T}
+    for threads, n in ((1, 1024), (T, 1024 * T)):
+        n = min(n, len(off) - 1)
+        a, c = base_in.copy(), base_out.copy()
+        t0 = time.perf_counter()
+        O.process_windows(a, c, off[:n + 1], ins[:off[n]], outs[:n], 0.025, SIGMOID_TABLE_F32,
+                          n_threads=threads)
+        dt = time.perf_counter() - t0
+        out[f"threads_{threads}"] = {"sample_windows": n, "windows_per_sec": n / dt,
+                                     "alg_GBps": float(wbytes[:n].sum()) / dt / 1e9,
+                                     "GFLOPs": float(wflops[:n].sum()) / dt / 1e9}
+    return out
+
+
 # --------------------------------------------------------------- GPU leg ----
 def micro_bench(args):
     """BASELINE.json configs[1]: sgns_update_windows on packed windows, snapshot mode.
 
     V = 100,000 fixed random rows ~ N(0, d^-1/2) (1% of rows x4 to hit the table clamps),
     inputs and targets ~ Zipf(1.0) over rows, negatives ~ Zipf^0.75 rejecting the target,
-    full windows (m = 2w; w = 10 uses one chunk of 20 = batch_cap >= 20 on both sides),
-    alpha = 0.025.  One JSON line per shape; algorithmic bytes 2(m+K+1)d4 per window.
+    full windows (m = 2w; w = 10 uses one chunk of 20 = batch_cap >= 20 on both sides)
+    plus one dynamic variant (m = 2b, b ~ U{1..w}), alpha = 0.025.  One JSON line per
+    shape; algorithmic bytes 2(m+K+1)d4 and flops 6m(K+1)d summed over the windows.
+    CPU leg (unless --no-cpu-baseline): the oracle's restatement of the reference core on
+    the same windows (first 1,024 on one thread; first 1,024 x T on T host threads,
+    Hogwild on contiguous ranges as the reference's threads).
     """
     import torch
     from paper_1604_04661_b200.kernel_batched import DeviceWindowBatch, WindowBatch, update_windows
@@ -234,31 +259,34 @@ def micro_bench(args):
     torch.cuda.set_device(0)
     peak, peak_kind = measured_peaks()
     V = 100_000
-    shapes = [(4096, 300, 5, 5), (16384, 300, 5, 5), (65536, 300, 5, 5), (65536, 100, 5, 5),
-              (65536, 200, 5, 5), (65536, 300, 2, 5), (65536, 300, 10, 5), (65536, 300, 5, 10),
-              (65536, 300, 5, 15), (65536, 100, 10, 15)]
+    shapes = [(4096, 300, 5, 5, False), (16384, 300, 5, 5, False), (65536, 300, 5, 5, False),
+              (65536, 100, 5, 5, False), (65536, 200, 5, 5, False), (65536, 300, 2, 5, False),
+              (65536, 300, 10, 5, False), (65536, 300, 5, 10, False), (65536, 300, 5, 15, False),
+              (65536, 100, 10, 15, False), (65536, 300, 5, 5, True)]
+    T = len(os.sched_getaffinity(0))
     rng = np.random.default_rng(args.seed)
     ranks = np.arange(1, V + 1, dtype=np.float64)
-    pz = 1.0 / ranks
+    pz = 1.0 / ranks if args.micro_ids == "zipf" else np.ones_like(ranks)
     pz /= pz.sum()
     pn = pz ** 0.75
     pn /= pn.sum()
-    for n_win, d, w, k in shapes:
+    for n_win, d, w, k, dyn in shapes:
         sig = d ** -0.25
         base_in = (rng.normal(size=(V, d)) * sig).astype(np.float32)
         base_out = (rng.normal(size=(V, d)) * sig).astype(np.float32)
         hot = rng.choice(V, V // 100, replace=False)
         base_in[hot] *= 4
-        m = 2 * w
-        ins = rng.choice(V, size=(n_win, m), p=pz).astype(np.int32)
+        ms = 2 * rng.integers(1, w + 1, size=n_win) if dyn else np.full(n_win, 2 * w)
+        off = np.concatenate([[0], np.cumsum(ms)]).astype(np.int32)
+        ins = rng.choice(V, size=int(off[-1]), p=pz).astype(np.int32)
         tgt = rng.choice(V, size=n_win, p=pz).astype(np.int32)
         negs = rng.choice(V, size=(n_win, k), p=pn).astype(np.int32)
         bad = negs == tgt[:, None]
         while bad.any():
             negs[bad] = rng.choice(V, size=int(bad.sum()), p=pn)
             bad = negs == tgt[:, None]
-        wb = WindowBatch(np.arange(0, n_win * m + 1, m, dtype=np.int32), ins.ravel(),
-                         np.concatenate([tgt[:, None], negs], axis=1).astype(np.int32))
+        outs = np.concatenate([tgt[:, None], negs], axis=1).astype(np.int32)
+        wb = WindowBatch(off, ins, outs)
         dwb = DeviceWindowBatch(wb)
         src = DeviceModel.from_host(EmbeddingModel(base_in, base_out))
         dst = src.clone()
@@ -275,14 +303,18 @@ def micro_bench(args):
             ev[i][1].record(st)
         torch.cuda.synchronize()
         t = float(np.mean([a.elapsed_time(b) for a, b in ev])) / 1e3
-        by = 2.0 * (m + k + 1) * d * 4 * n_win
-        fl = 6.0 * m * (k + 1) * d * n_win
-        print(json.dumps({"mode": "micro", "n_windows": n_win, "dim": d, "window": w, "negatives": k,
-                          "inputs_per_window": m, "us_per_launch": t * 1e6,
-                          "windows_per_sec": n_win / t, "alg_GBps": by / t / 1e9,
-                          "frac_of_peak": by / t / 1e9 / peak, "peak": peak, "peak_source": peak_kind,
-                          "GFLOPs": fl / t / 1e9, "l2": "flushed (256 MB write) before every launch"}),
-              flush=True)
+        wbytes = 2.0 * (ms + k + 1) * d * 4
+        wflops = 6.0 * ms * (k + 1) * d
+        by, fl = float(wbytes.sum()), float(wflops.sum())
+        line = {"mode": "micro", "n_windows": n_win, "dim": d, "window": w, "negatives": k,
+                "windows": "dynamic m=2b, b~U{1..w}" if dyn else "full m=2w",
+                "inputs_per_window": float(ms.mean()), "us_per_launch": t * 1e6,
+                "windows_per_sec": n_win / t, "alg_GBps": by / t / 1e9,
+                "frac_of_peak": by / t / 1e9 / peak, "peak": peak, "peak_source": peak_kind,
+                "GFLOPs": fl / t / 1e9, "l2": "flushed (256 MB write) before every launch"}
+        if not args.no_cpu_baseline:
+            line["cpu_reference"] = micro_cpu_leg(base_in, base_out, off, ins, outs, wbytes, wflops, T)
+        print(json.dumps(line), flush=True)
         del src, dst, dwb, flush
         torch.cuda.empty_cache()
 

@@ -69,6 +69,8 @@ _lib.or_sigmoid_table_f32.restype = C.c_float
 _lib.or_sigmoid_table_f32.argtypes = [C.c_float, P]
 _lib.or_process_batch.argtypes = [C.c_int, P, P, I64, C.c_int, P, C.c_int, P, C.c_int, F64,
                                   C.c_int, P]
+_lib.or_process_windows.argtypes = [C.c_int, P, P, I64, C.c_int, P, P, P, I64, C.c_int, F64,
+                                    C.c_int, P, C.c_int]
 _lib.or_init_model.argtypes = [I64, C.c_int, U64, P]
 _lib.or_neg_boundaries.argtypes = [P, I64, F64, I64, P]
 _lib.or_drive.argtypes = [C.POINTER(Drive), C.c_int]
@@ -118,6 +120,25 @@ def process_batch(m_in: np.ndarray, m_out: np.ndarray, in_ids, out_ids, alpha: f
     tab = np.ascontiguousarray(table, dtype=m_in.dtype)
     _lib.or_process_batch(dtype, _p(m_in), _p(m_out), m_in.shape[1], m_in.shape[1], _p(ins),
                           len(ins), _p(outs), len(outs), float(alpha), dtype, _p(tab))
+
+
+def process_windows(m_in: np.ndarray, m_out: np.ndarray, in_off, in_ids, out_ids, alpha: float,
+                    table: np.ndarray, n_threads: int = 1) -> None:
+    """Packed windows in place (out_ids n_win x K1); n_threads Hogwild threads on contiguous
+    window ranges; one thread == sequential process_batch calls."""
+    assert m_in.flags.c_contiguous and m_out.flags.c_contiguous and m_in.dtype == m_out.dtype
+    dtype = 1 if m_in.dtype == np.float64 else 0
+    off = np.ascontiguousarray(in_off, dtype=np.int32)
+    ins = np.ascontiguousarray(in_ids, dtype=np.int32)
+    outs = np.ascontiguousarray(out_ids, dtype=np.int32)
+    tab = np.ascontiguousarray(table, dtype=m_in.dtype)
+    n_win = len(off) - 1
+    k1 = outs.size // max(n_win, 1)
+    assert outs.size == n_win * k1
+    if _lib.or_process_windows(dtype, _p(m_in), _p(m_out), m_in.shape[1], m_in.shape[1], _p(off),
+                               _p(ins), _p(outs), n_win, k1, float(alpha), dtype, _p(tab),
+                               int(n_threads)) != 0:
+        raise MemoryError("or_process_windows")
 
 
 def init_model(V: int, D: int, seed: int) -> np.ndarray:

@@ -84,6 +84,35 @@ def test_process_batch_naive_bitwise(dtype):
         np.testing.assert_allclose(c[r_out], g[f"c{i}_{dtype}_blas_mout"], rtol=2e-5, atol=1e-7)
 
 
+def test_process_windows_is_sequential_process_batch():
+    """The microbench CPU leg: one thread == the windows through process_batch in order;
+    T threads on disjoint rows == the same result (no row is shared)."""
+    rng = np.random.default_rng(5)
+    V, D, K1 = 300, 24, 6
+    tab = load_golden("tables")["sigmoid_f32"]
+    m_in = rng.normal(size=(V, D)).astype(np.float32) * 0.3
+    m_out = rng.normal(size=(V, D)).astype(np.float32) * 0.3
+    ms = rng.integers(1, 11, size=40)
+    off = np.concatenate([[0], np.cumsum(ms)]).astype(np.int32)
+    ins = rng.integers(0, V, size=off[-1]).astype(np.int32)
+    outs = rng.integers(0, V, size=(40, K1)).astype(np.int32)
+    a, c = m_in.copy(), m_out.copy()
+    for w in range(40):
+        O.process_batch(a, c, ins[off[w]:off[w + 1]], outs[w], 0.025, tab)
+    b, d = m_in.copy(), m_out.copy()
+    O.process_windows(b, d, off, ins, outs, 0.025, tab, n_threads=1)
+    assert np.array_equal(a, b) and np.array_equal(c, d)
+    # disjoint rows: window w uses rows [w*7, w*7+7)
+    ins2 = np.concatenate([np.arange(w * 7, w * 7 + 1) for w in range(40)]).astype(np.int32)
+    off2 = np.arange(41, dtype=np.int32)
+    outs2 = np.array([np.arange(w * 7 + 1, w * 7 + 7) for w in range(40)], np.int32)
+    a, c = m_in.copy(), m_out.copy()
+    O.process_windows(a, c, off2, ins2, outs2, 0.025, tab, n_threads=1)
+    b, d = m_in.copy(), m_out.copy()
+    O.process_windows(b, d, off2, ins2, outs2, 0.025, tab, n_threads=4)
+    assert np.array_equal(a, b) and np.array_equal(c, d)
+
+
 @pytest.mark.parametrize("case", TRACE_CASES, ids=[c[0] for c in TRACE_CASES])
 def test_driver_stream_matches_reference_pipeline(case):
     """Windows, chunks and shared negatives: bit-exact vs subsample->iterate_windows->assemble_batches."""
