@@ -459,7 +459,9 @@ def main():
     # ---- e2e: the public streaming API from pinned host buffers (H2D + D2H in the timed region)
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_leg(args, corpus, enc, shard, cfg, counts, keep, world, rank, dev, alpha0_eff, total_x)
+        period_index[0] = 0
+        e2e = e2e_leg(args, corpus, enc, shard, cfg, counts, keep, world, rank, dev, alpha0_eff, total_x,
+                      transport=transport, sync_rows=sync_rows)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -481,9 +483,11 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_leg(args, corpus, enc, shard, cfg, counts, keep, world, rank, dev, alpha0_eff, total_x):
+def e2e_leg(args, corpus, enc, shard, cfg, counts, keep, world, rank, dev, alpha0_eff, total_x,
+            transport=None, sync_rows=None):
     """Same metric through the public streaming API: each step copies its ~1M-token
-    sentence chunk from pinned host memory, trains it, and reads back its counters."""
+    sentence chunk from pinned host memory, trains it, reads back its counters, and
+    (N > 1) averages the same rows as the device-timed leg between chunks."""
     import torch
     import torch.distributed as dist
     from paper_1604_04661_b200.model import init_device_model
@@ -509,6 +513,12 @@ def e2e_leg(args, corpus, enc, shard, cfg, counts, keep, world, rank, dev, alpha
                           alpha0_eff=alpha0_eff, keep_probs=keep)
     stream = torch.cuda.current_stream(dev)
 
+    def sync():
+        rows = sync_rows()
+        transport.allreduce_average(model.m_in, rows, "in")
+        transport.allreduce_average(model.m_out, rows, "out")
+    after = sync if transport is not None else None
+
     off_pinned = torch.from_numpy(np.ascontiguousarray(off, dtype=np.int64)).pin_memory()
 
     def chunks(lo, hi):
@@ -517,7 +527,7 @@ def e2e_leg(args, corpus, enc, shard, cfg, counts, keep, world, rank, dev, alpha
             base = int(off[a])
             yield (host_ids[base - tok_lo:int(off[b]) - tok_lo], off_pinned[a:b + 1] - base, base)
 
-    for _ in st.train_chunks(chunks(0, args.warmup)):
+    for _ in st.train_chunks(chunks(0, args.warmup), after_launch=after):
         pass
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -527,7 +537,7 @@ def e2e_leg(args, corpus, enc, shard, cfg, counts, keep, world, rank, dev, alpha
     wall0 = time.perf_counter()
     trained = 0
     h2d = d2h = 0
-    for tr, rd, ls, cl, inp, ch in st.train_chunks(chunks(args.warmup, n_chunks)):
+    for tr, rd, ls, cl, inp, ch in st.train_chunks(chunks(args.warmup, n_chunks), after_launch=after):
         trained += tr
         h2d += st.h2d_bytes
         d2h += st.d2h_bytes

@@ -622,9 +622,12 @@ class StreamingTrainer:
         # (words_trained, words_read, loss_sum, loss_cells, inputs, chunks)
         return int(a[0]), int(a[1]), loss, int(a[4]), int(a[3]), int(a[2])
 
-    def train_chunks(self, chunks):
+    def train_chunks(self, chunks, after_launch=None):
         """Train an iterable of (ids_host, offsets_host, token_base[, epoch[, words_base]])
-        chunks with copy/compute overlap; yields each chunk's counters in order."""
+        chunks with copy/compute overlap; yields each chunk's counters in order.
+        `after_launch()`, if given, runs after each chunk's kernel is enqueued and before
+        the next one is: stream-ordered work between chunks (the data-parallel model
+        average, sgns/distributed.py:470-472)."""
         it = iter(chunks)
         try:
             nxt = next(it)
@@ -643,6 +646,8 @@ class StreamingTrainer:
                 epoch = cur[3] if len(cur) > 3 else 0
                 words_base = cur[4] if len(cur) > 4 else cur[2]
                 self._launch(cur_buf, cur_staged[0], cur_staged[1], cur[2], epoch, words_base)
+            if after_launch is not None:
+                after_launch()
             if nxt is not None:
                 buf ^= 1
                 staged = self._stage(buf, nxt[0], nxt[1])

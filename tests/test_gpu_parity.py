@@ -174,15 +174,17 @@ def test_disjoint_windows_equal_sequential(dtype, D, k):
         assert bad_rows <= flips * 16, (bad_rows, flips)
 
 
-@pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_snapshot_conflicting_windows(dtype):
-    """P3: Zipf-conflicting windows in snapshot mode == snapshot + sum of per-window deltas."""
+@pytest.mark.parametrize("dtype,D,k", [("f64", 300, 5), ("f32", 300, 5), ("f32", 100, 12),
+                                       ("f32", 64, 7)])
+def test_snapshot_conflicting_windows(dtype, D, k):
+    """P3: Zipf-conflicting windows in snapshot mode == snapshot + sum of per-window deltas
+    (float32: the hottest rows' adds are combined in shared memory per CTA first)."""
     P, O = _pkg(), _oracle()
     from paper_1604_04661_b200.kernel_batched import DeviceWindowBatch, WindowBatch
     from paper_1604_04661_b200.model import DeviceModel, SIGMOID_TABLE_F32, SIGMOID_TABLE_F64
-    rng = np.random.default_rng(7)
+    rng = np.random.default_rng(7 + D + k)
     npdt = np.float64 if dtype == "f64" else np.float32
-    V, D, k = 500, 300, 5
+    V = 500
     base = P.EmbeddingModel((rng.normal(size=(V, D)) * D ** -0.25).astype(npdt),
                             (rng.normal(size=(V, D)) * D ** -0.25).astype(npdt))
     wins = _random_windows(rng, V, 400, 10, k)
@@ -424,3 +426,38 @@ def test_streaming_chunks_equal_resident_training():
     a, b = dm1.to_host(), dm2.to_host()
     np.testing.assert_allclose(b.input_vectors, a.input_vectors, rtol=0, atol=1e-6)
     np.testing.assert_allclose(b.output_vectors, a.output_vectors, rtol=0, atol=1e-6)
+
+
+def test_streaming_after_launch_hook_is_stream_ordered():
+    """train_chunks(after_launch=f) runs f between chunk i's kernel and chunk i+1's (the
+    data-parallel average slot): model snapshots taken by the hook equal the state after
+    training chunks 0..i one at a time."""
+    P = _pkg()
+    from paper_1604_04661_b200.synthetic import make_planted_corpus
+    from paper_1604_04661_b200.model import DeviceModel
+    from paper_1604_04661_b200.trainer import StreamingTrainer
+    syn = make_planted_corpus(30_000, 400, n_clusters=4, cluster_size=5, sentence_len=29, seed=3)
+    ids, off, counts = syn.encoded.ids, syn.encoded.offsets, syn.vocab.counts
+    V, D = len(counts), 32
+    base = np.random.default_rng(2).normal(size=(V, D)).astype(np.float32) * 0.1
+    cfg = P.TrainingConfig(dim=D, window=4, negatives=5, subsample=1e-3, min_count=1, seed=5,
+                           epochs=1, workers=1)
+    cuts = [0, 200, 450, 700, len(off) - 1]
+    host_ids = torch.from_numpy(ids).pin_memory()
+    chunks = [(host_ids[off[a]:off[b]], off[a:b + 1] - off[a], int(off[a])) for a, b in zip(cuts, cuts[1:])]
+
+    def trainer():
+        dm = DeviceModel.from_host(P.EmbeddingModel(base.copy(), np.zeros_like(base)))
+        return dm, StreamingTrainer(dm, counts, cfg, float(off[-1]), 20_000, 2_000,
+                                    syn.encoded.max_sentence_length(), n_workers=1)
+    dm1, st1 = trainer()
+    want = []
+    for c in chunks:
+        st1.train_chunk(*c)
+        want.append(dm1.m_out.clone())
+    dm2, st2 = trainer()
+    got = []
+    res = list(st2.train_chunks(chunks, after_launch=lambda: got.append(dm2.m_out.clone())))
+    assert len(res) == len(got) == len(chunks)
+    for w, g in zip(want, got):
+        torch.testing.assert_close(g, w, rtol=0, atol=1e-6)
