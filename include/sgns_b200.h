@@ -61,7 +61,8 @@ typedef struct sgns_worker {
 
 /* One batch of packed windows (the CSR form of a list of Minibatch,
  * kernel_batched.py:37-54): window w has inputs in_ids[in_off[w]:in_off[w+1]]
- * and outputs out_ids[w*k1 : (w+1)*k1], target first. */
+ * and outputs out_ids[w*k1 : (w+1)*k1], target first.  n_windows == 0 is a no-op
+ * (SGNS_OK before any pointer is inspected). */
 int sgns_update_windows(
     int32_t dtype,
     void *d_m_in_dst, void *d_m_out_dst,              /* rows receive += deltas */

@@ -185,8 +185,14 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
   int *bw_s = reinterpret_cast<int *>(base + L.bw);
   const int idsn = mcap + K1R;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const int64_t ld = p.mv.ld;
+  const int ld = (int)p.mv.ld;  // shared-memory indexing in 32 bits
   const int nvec = p.mv.nvec, nslot = 2 * nvec;
+  // lane offsets folded into the model base pointers once: every gather/scatter below is
+  // base + 32-bit row offset + a compile-time slot offset
+  float *const in_dst_l = p.mv.in_dst + 2 * lane;
+  float *const out_dst_l = p.mv.out_dst + 2 * lane;
+  const float *const out_src_l = p.mv.out_src + 2 * lane;
+  const float *const in_src_l = p.mv.in_src + 4 * lane;
   auto slot_ok = [&](int j) { return FULL || j < NS - 1 || lane + 32 * j < nslot; };
   auto chunk_ok = [&](int j) { return j < NCH - 1 || lane + 32 * j < nvec; };
   auto kk_ok = [&](int k) { return EXACT_K || k < k1; };
@@ -295,10 +301,10 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
       const uint32_t *off_s = roff_b;
 #pragma unroll
       for (int k = 0; k < K1R; ++k) {
-        const float *src = p.mv.out_src + off_s[u.mc + (kk_ok(k) ? k : 0)];
+        const float *src = out_src_l + off_s[u.mc + (kk_ok(k) ? k : 0)];
 #pragma unroll
         for (int j = 0; j < NS; ++j)
-          c_reg[k][j] = (kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 2 * (lane + 32 * j)) : f2zero();
+          c_reg[k][j] = (kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 64 * j) : f2zero();
       }
     }
     bool have = true;
@@ -310,11 +316,11 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
       const int m = u.mc;
       // A rows of u -> smem
       for (int r = 0; r < m; ++r) {
-        const float *src = p.mv.in_src + off_s[r];
-        float *dst = rows_s + (int64_t)r * ld;
+        const float *src = in_src_l + off_s[r];
+        float *dst = rows_s + r * ld + 4 * lane;
 #pragma unroll
         for (int j = 0; j < NCH; ++j)
-          if (chunk_ok(j)) cp_async16(dst + (lane + 32 * j) * 4, src + (lane + 32 * j) * 4);
+          if (chunk_ok(j)) cp_async16(dst + 128 * j, src + 128 * j);
       }
       // next unit + its negative candidates (alias loads in flight during u's math)
       Unit nx;
@@ -361,7 +367,7 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
           float2 a[NS];
 #pragma unroll
           for (int j = 0; j < NS; ++j)
-            a[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)ii * ld + 2 * (lane + 32 * j))
+            a[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + ii * ld + 2 * (lane + 32 * j))
                               : f2zero();
 #pragma unroll
           for (int k = 0; k < NV; ++k) {
@@ -399,11 +405,10 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
             for (int j = 0; j < NS; ++j)
               d[j] = k == 0 ? __fmul2_rn(ek2, c_reg[0][j]) : __ffma2_rn(ek2, c_reg[k][j], d[j]);
           }
-          float *dst = p.mv.in_dst + off_s[i + h];
+          float *dst = in_dst_l + off_s[i + h];
 #pragma unroll
           for (int j = 0; j < NS; ++j)
-            if (slot_ok(j))
-              atomicAdd(reinterpret_cast<float2 *>(dst + 2 * (lane + 32 * j)), __fmul2_rn(d[j], alpha2));
+            if (slot_ok(j)) atomicAdd(reinterpret_cast<float2 *>(dst + 64 * j), __fmul2_rn(d[j], alpha2));
         }
       }
       // C registers are free: finish u+1's negatives and start loading its output rows
@@ -427,10 +432,10 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < K1R; ++k) {
-          const float *src = p.mv.out_src + off_n[nx.mc + (kk_ok(k) ? k : 0)];
+          const float *src = out_src_l + off_n[nx.mc + (kk_ok(k) ? k : 0)];
 #pragma unroll
           for (int j = 0; j < NS; ++j)
-            c_reg[k][j] = (kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 2 * (lane + 32 * j)) : f2zero();
+            c_reg[k][j] = (kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 64 * j) : f2zero();
         }
       }
       __syncwarp();
@@ -440,7 +445,7 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
       float *orow[K1R];
 #pragma unroll
       for (int k = 0; k < K1R; ++k)
-        orow[k] = p.mv.out_dst + off_s[m + (kk_ok(k) ? k : 0)] + 2 * lane;
+        orow[k] = out_dst_l + off_s[m + (kk_ok(k) ? k : 0)];
 #pragma unroll
       for (int j = 0; j < NS; ++j) {
         if (!slot_ok(j)) continue;
@@ -448,10 +453,12 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
         float2 acc[K1R];
 #pragma unroll
         for (int k = 0; k < K1R; ++k) acc[k] = f2zero();
-        for (int i = 0; i < m; ++i) {
-          const float2 a0 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col);
-          const float4 e03 = *reinterpret_cast<const float4 *>(e_s + i * 8);
-          const float4 e47 = *reinterpret_cast<const float4 *>(e_s + i * 8 + 4);
+        const float *ap = rows_s + col;
+        const float *ep = e_s;
+        for (int i = 0; i < m; ++i, ap += ld, ep += 8) {
+          const float2 a0 = *reinterpret_cast<const float2 *>(ap);
+          const float4 e03 = *reinterpret_cast<const float4 *>(ep);
+          const float4 e47 = *reinterpret_cast<const float4 *>(ep + 4);
           const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
 #pragma unroll
           for (int k = 0; k < K1R; ++k)

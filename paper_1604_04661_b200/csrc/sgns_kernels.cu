@@ -872,10 +872,10 @@ int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, cons
                         int32_t n_windows, int32_t k1, int32_t max_inputs, const void *d_alpha,
                         const void *d_sig_table, int32_t sigmoid_mode, int32_t loss_every,
                         double *d_loss_sum, int64_t *d_loss_cells, int32_t *d_error, void *stream) {
+  if (n_windows == 0) return SGNS_OK;  // an empty packed batch is a no-op (empty id arrays may be null)
   if (!d_m_in_dst || !d_m_out_dst || !d_m_in_src || !d_m_out_src || !d_in_off || !d_in_ids ||
       !d_out_ids || !d_alpha || !d_sig_table || vocab < 1)
     return SGNS_E_ARG;
-  if (n_windows == 0) return SGNS_OK;
   if (n_windows < 0 || max_inputs < 1 || k1 < 2 || k1 > kMaxK1 || !ld_ok(dtype, dim, ld))
     return SGNS_E_SHAPE;
   if (loss_every > 0 && (!d_loss_sum || !d_loss_cells)) return SGNS_E_ARG;

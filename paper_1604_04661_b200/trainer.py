@@ -192,7 +192,6 @@ class DeviceSampler:
 
     def __init__(self, counts: np.ndarray, rng: str, table_length: int | None = None,
                  table: NegativeTable | None = None, device="cuda", power: float = NEGATIVE_POWER):
-        torch = _torch()
         self.rng = rng
         counts = np.ascontiguousarray(counts, dtype=np.int64)
         V = len(counts)
@@ -207,6 +206,14 @@ class DeviceSampler:
                     from .corpus import TableLengthError
                     raise TableLengthError(f"table length {L} is smaller than vocabulary size {V}")
                 bounds = negative_table_boundaries(counts, power, L)
+            if np.count_nonzero(np.diff(bounds, prepend=0)) < 2:
+                raise ValueError("negative table holds fewer than two distinct words: every draw "
+                                 "would equal the target (the reference's rejection loop never ends)")
+        elif np.count_nonzero(counts > 0) < 2:
+            raise ValueError("fewer than two words with a positive count: no negative can "
+                             "differ from the target")
+        torch = _torch()
+        if rng == "splitmix":
             n = int(bounds[-1])
             d_bounds = torch.from_numpy(bounds).to(device)
             self.slots = torch.empty(n, dtype=torch.int32, device=device)

@@ -33,6 +33,8 @@ def test_device_entry_points_validate_before_launch():
     L = _lib.lib()
     assert L.sgns_update_windows(0, None, None, None, None, 1, 4, 4, None, None, None, 1, 2, 1,
                                  None, None, 0, 0, None, None, None, None) == -1
+    assert L.sgns_update_windows(0, None, None, None, None, 1, 4, 4, None, None, None, 0, 2, 1,
+                                 None, None, 0, 0, None, None, None, None) == 0  # empty batch
     assert L.sgns_drive(None, None) == -1
     assert L.sgns_init_model(0, None, None, 1, 4, 4, 0, None) == -1
     assert L.sgns_init_model(0, 1, 1, 1, 3, 3, 0, None) == -2  # row not a multiple of 16 bytes
@@ -142,3 +144,13 @@ def test_eval_similarity_matches_reference():
     assert [used, skipped] == e["rho"][1:].astype(int).tolist()
     assert rho == pytest.approx(float(e["rho"][0]), abs=1e-9)
     del names
+
+
+def test_sampler_rejects_tables_without_a_second_word():
+    """A negative table with one distinct word would make the target-rejection loop spin
+    forever on the device (the reference hangs the same way); refuse it up front."""
+    from paper_1604_04661_b200.trainer import DeviceSampler
+    with pytest.raises(ValueError):
+        DeviceSampler(np.array([7, 0, 0]), "philox", device="cpu")
+    with pytest.raises(ValueError):
+        DeviceSampler(np.array([5, 0]), "splitmix", table_length=10, device="cpu")
