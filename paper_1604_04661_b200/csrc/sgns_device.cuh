@@ -334,43 +334,60 @@ __device__ __forceinline__ float2 ld_cg_f2(const float *p) {
   return v;
 }
 
-template <int NS, int NCH, int K1R, bool EXACT_K>
-__device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, const uint32_t *off_s,
-                                                 int m, int k1, float alpha, bool exact,
-                                                 const float *sig_s, bool want_loss,
-                                                 double &loss_acc, long long &cell_acc,
-                                                 float *rows_s, float *e_s, int lane) {
-  constexpr int NV = 8;
-  static_assert(K1R <= NV, "K1R <= 8");
-  if constexpr (EXACT_K) k1 = K1R;
-  const int64_t ld = mv.ld;
-  const int nvec = mv.nvec;    // 16-byte chunks per row
-  const int nslot = nvec * 2;  // 8-byte slots per row
+// The float32 k1 <= 8 window update in four phases:
+//   f2_issue_a   input rows -> smem (16-byte cp.async)
+//   f2_load_c    output rows -> registers (8-byte L2 loads)
+//   f2_score_da  wait for the rows; scores, errors (to e_s), dA scattered
+//   f2_dc        dC_k = sum_i (alpha err_ik) A_i, column-outer over the staged rows
+template <int NS, int NCH> struct F2Shape {
+  int ld, nvec, nslot, lane;
+  __device__ F2Shape(const ModelView<float> &mv, int lane_)
+      : ld((int)mv.ld), nvec(mv.nvec), nslot(2 * mv.nvec), lane(lane_) {}
   // slot j of this lane is always in range for j < NS - 1 (NS = ceil(nslot / 32))
-  auto slot_ok = [&](int j) { return j < NS - 1 || lane + 32 * j < nslot; };
-  auto chunk_ok = [&](int j) { return j < NCH - 1 || lane + 32 * j < nvec; };
-  auto kk_ok = [&](int k) { return EXACT_K || k < k1; };
+  __device__ bool slot_ok(int j) const { return j < NS - 1 || lane + 32 * j < nslot; }
+  __device__ bool chunk_ok(int j) const { return j < NCH - 1 || lane + 32 * j < nvec; }
+};
 
-  // 1. gathers: input rows -> smem (16-byte cp.async), output rows -> registers (8-byte L2 loads)
+template <int NS, int NCH>
+__device__ __forceinline__ void f2_issue_a(const ModelView<float> &mv, const F2Shape<NS, NCH> &sh,
+                                           const uint32_t *off_s, int m, float *rows_s) {
+  const float *src_l = mv.in_src + 4 * sh.lane;
   for (int r = 0; r < m; ++r) {
-    const float *src = mv.in_src + off_s[r];
-    float *dst = rows_s + (int64_t)r * ld;
+    const float *src = src_l + off_s[r];
+    float *dst = rows_s + r * sh.ld + 4 * sh.lane;
 #pragma unroll
     for (int j = 0; j < NCH; ++j)
-      if (chunk_ok(j)) cp_async16(dst + (lane + 32 * j) * 4, src + (lane + 32 * j) * 4);
+      if (sh.chunk_ok(j)) cp_async16(dst + 128 * j, src + 128 * j);
   }
-  float2 c[K1R][NS];
+}
+
+template <int NS, int NCH, int K1R, bool EXACT_K>
+__device__ __forceinline__ void f2_load_c(float2 (&c)[K1R][NS], const ModelView<float> &mv,
+                                          const F2Shape<NS, NCH> &sh, const uint32_t *off_out,
+                                          int k1) {
+  const float *src_l = mv.out_src + 2 * sh.lane;
 #pragma unroll
   for (int k = 0; k < K1R; ++k) {
-    const float *src = mv.out_src + off_s[m + (kk_ok(k) ? k : 0)];
+    const bool kk = EXACT_K || k < k1;
+    const float *src = src_l + off_out[kk ? k : 0];
 #pragma unroll
-    for (int j = 0; j < NS; ++j)
-      c[k][j] = (kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 2 * (lane + 32 * j)) : f2zero();
+    for (int j = 0; j < NS; ++j) c[k][j] = (kk && sh.slot_ok(j)) ? ld_cg_f2(src + 64 * j) : f2zero();
   }
+}
+
+template <int NS, int NCH, int K1R, bool EXACT_K>
+__device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const ModelView<float> &mv,
+                                            const F2Shape<NS, NCH> &sh, const uint32_t *off_s,
+                                            int m, int k1, float alpha, bool exact,
+                                            const float *sig_s, bool want_loss, double &loss_acc,
+                                            long long &cell_acc, const float *rows_s, float *e_s) {
+  constexpr int NV = 8;
+  static_assert(K1R <= NV, "K1R <= 8");
+  const int lane = sh.lane;
   cp_async_wait_all();
   __syncwarp();  // staged rows were copied in 16-byte lanes, read in 8-byte lanes
-
   const float2 alpha2 = make_float2(alpha, alpha);
+  float *in_dst_l = mv.in_dst + 2 * lane;
   // inputs in pairs: one transposed butterfly over 16 values reduces both inputs' scores
   for (int i = 0; i < m; i += 2) {
     const bool two = i + 1 < m;
@@ -381,8 +398,8 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
       float2 a[NS];
 #pragma unroll
       for (int j = 0; j < NS; ++j)
-        a[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)ii * ld + 2 * (lane + 32 * j))
-                          : f2zero();
+        a[j] = sh.slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + ii * sh.ld + 2 * (lane + 32 * j))
+                             : f2zero();
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
         if (k < K1R) {
@@ -421,26 +438,34 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
 #pragma unroll
         for (int j = 0; j < NS; ++j) d[j] = k == 0 ? __fmul2_rn(ek2, c[0][j]) : __ffma2_rn(ek2, c[k][j], d[j]);
       }
-      float *dst = mv.in_dst + off_s[i + h];
+      float *dst = in_dst_l + off_s[i + h];
 #pragma unroll
       for (int j = 0; j < NS; ++j)
-        if (slot_ok(j))
-          atomicAdd(reinterpret_cast<float2 *>(dst + 2 * (lane + 32 * j)), __fmul2_rn(d[j], alpha2));
+        if (sh.slot_ok(j)) atomicAdd(reinterpret_cast<float2 *>(dst + 64 * j), __fmul2_rn(d[j], alpha2));
     }
   }
   __syncwarp();
-  // dC_k = sum_i (alpha err_ik) A_i, column-outer over the staged rows
+}
+
+template <int NS, int NCH, int K1R, bool EXACT_K>
+__device__ __forceinline__ void f2_dc(const ModelView<float> &mv, const F2Shape<NS, NCH> &sh,
+                                      const uint32_t *off_s, int m, int k1, const float *rows_s,
+                                      const float *e_s) {
+  auto kk_ok = [&](int k) { return EXACT_K || k < k1; };
+  float *out_dst_l = mv.out_dst + 2 * sh.lane;
 #pragma unroll
   for (int j = 0; j < NS; ++j) {
-    if (!slot_ok(j)) continue;
-    const int col = 2 * (lane + 32 * j);
+    if (!sh.slot_ok(j)) continue;
+    const int col = 2 * (sh.lane + 32 * j);
     float2 acc[K1R];
 #pragma unroll
     for (int k = 0; k < K1R; ++k) acc[k] = f2zero();
-    for (int i = 0; i < m; ++i) {
-      const float2 a0 = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col);
-      const float4 e03 = *reinterpret_cast<const float4 *>(e_s + i * 8);
-      const float4 e47 = *reinterpret_cast<const float4 *>(e_s + i * 8 + 4);
+    const float *ap = rows_s + col;
+    const float *ep = e_s;
+    for (int i = 0; i < m; ++i, ap += sh.ld, ep += 8) {
+      const float2 a0 = *reinterpret_cast<const float2 *>(ap);
+      const float4 e03 = *reinterpret_cast<const float4 *>(ep);
+      const float4 e47 = *reinterpret_cast<const float4 *>(ep + 4);
       const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
 #pragma unroll
       for (int k = 0; k < K1R; ++k)
@@ -448,9 +473,25 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
     }
 #pragma unroll
     for (int k = 0; k < K1R; ++k)
-      if (kk_ok(k)) atomicAdd(reinterpret_cast<float2 *>(mv.out_dst + off_s[m + k] + col), acc[k]);
+      if (kk_ok(k)) atomicAdd(reinterpret_cast<float2 *>(out_dst_l + off_s[m + k] + 64 * j), acc[k]);
   }
   __syncwarp();
+}
+
+template <int NS, int NCH, int K1R, bool EXACT_K>
+__device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, const uint32_t *off_s,
+                                                 int m, int k1, float alpha, bool exact,
+                                                 const float *sig_s, bool want_loss,
+                                                 double &loss_acc, long long &cell_acc,
+                                                 float *rows_s, float *e_s, int lane) {
+  if constexpr (EXACT_K) k1 = K1R;
+  const F2Shape<NS, NCH> sh(mv, lane);
+  f2_issue_a<NS, NCH>(mv, sh, off_s, m, rows_s);
+  float2 c[K1R][NS];
+  f2_load_c<NS, NCH, K1R, EXACT_K>(c, mv, sh, off_s + m, k1);
+  f2_score_da<NS, NCH, K1R, EXACT_K>(c, mv, sh, off_s, m, k1, alpha, exact, sig_s, want_loss, loss_acc,
+                                     cell_acc, rows_s, e_s);
+  f2_dc<NS, NCH, K1R, EXACT_K>(mv, sh, off_s, m, k1, rows_s, e_s);
 }
 
 
