@@ -78,52 +78,88 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region."""
+    """SM clock and throttle reasons sampled during the timed region: NVML every 5 ms from
+    a background thread (the main thread sits in CUDA synchronisation), else nvidia-smi
+    every 50 ms.  LOCAL_RANK's device index is the NVML index (one process per GPU)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
-        self.path = tempfile.mktemp(suffix=".csv")
-        self.proc = None
         self.index = index
+        self.proc = None
+        self.thread = None
+        self.sm, self.smax, self.reasons = [], [], set()
+
+    def _nvml_loop(self, nv, handle, bits):
+        import time as _t
+        while not self.stop_flag:
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(handle, nv.NVML_CLOCK_SM)))
+                self.smax.append(float(nv.nvmlDeviceGetMaxClockInfo(handle, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(handle)
+                for name, bit in zip(self.NAMES, bits):
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001 - a failed sample is skipped
+                pass
+            _t.sleep(0.005)
 
     def start(self):
         try:
+            import threading
+            import pynvml as nv
+            nv.nvmlInit()
+            handle = nv.nvmlDeviceGetHandleByIndex(self.index)
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            self.stop_flag = False
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, handle, bits), daemon=True)
+            self.thread.start()
+            self.source = "nvml 5 ms"
+            return
+        except Exception:  # noqa: BLE001 - fall back to nvidia-smi
+            self.thread = None
+        try:
+            self.path = tempfile.mktemp(suffix=".csv")
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.fh,
                 stderr=subprocess.DEVNULL)
+            self.source = "nvidia-smi 50 ms"
         except OSError:
             self.proc = None
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        self.proc.wait()
-        self.fh.close()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        with open(self.path) as fh:
-            for line in fh:
-                f = [x.strip() for x in line.split(",")]
-                if len(f) < 6:
-                    continue
-                try:
-                    sm.append(float(f[0]))
-                    smax.append(float(f[1]))
-                except ValueError:
-                    continue
-                for n, v in zip(names, f[2:6]):
-                    if v.lower() == "active":
-                        reasons.add(n)
-        os.unlink(self.path)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": float(max(smax)) if smax else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        if self.thread is not None:
+            self.stop_flag = True
+            self.thread.join()
+        elif self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+            self.fh.close()
+            with open(self.path) as fh:
+                for line in fh:
+                    f = [x.strip() for x in line.split(",")]
+                    if len(f) < 6:
+                        continue
+                    try:
+                        self.sm.append(float(f[0]))
+                        self.smax.append(float(f[1]))
+                    except ValueError:
+                        continue
+                    for n, v in zip(self.NAMES, f[2:6]):
+                        if v.lower() == "active":
+                            self.reasons.add(n)
+            os.unlink(self.path)
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None,
+                "sm_max_mhz": float(max(self.smax)) if self.smax else None,
+                "samples": len(self.sm), "source": self.source, "reasons": sorted(self.reasons)}
 
 
 def build_corpus(args, device):
