@@ -491,6 +491,11 @@ def main():
     if os.path.exists(traffic_path):
         with open(traffic_path) as fh:
             roofline["traffic"] = json.load(fh).get("dram_bytes_per_launch")
+        if roofline["traffic"]:
+            # the same launch time against the DRAM bytes ncu measured: what HBM actually
+            # moved (hot rows hit in L2, so this is well below the algorithmic figure)
+            roofline["dram_achieved"] = roofline["traffic"] / avg_kernel_s / 1e9
+            roofline["dram_frac"] = roofline["dram_achieved"] / peak
 
     # ---- e2e: the public streaming API from pinned host buffers (H2D + D2H in the timed region)
     e2e = None

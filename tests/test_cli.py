@@ -65,3 +65,35 @@ def test_cli_train_writes_vectors_and_report(tmp_path):
     from paper_1604_04661_b200.model import load_model
     m, v = load_model(str(out))
     assert m.input_vectors.shape == (syn.vocab.size, 32) and np.isfinite(m.input_vectors).all()
+
+
+@pytest.mark.gpu
+def test_cli_train_dist_under_torchrun(tmp_path):
+    """train-dist through torchrun (one process per GPU, NCCL, rendezvous on 127.0.0.1):
+    a world of one rank trains, writes the vectors and the rank-0 report."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import socket
+    from paper_1604_04661_b200.synthetic import make_planted_corpus
+    syn = make_planted_corpus(40_000, 400, n_clusters=4, cluster_size=6, seed=5)
+    corpus = tmp_path / "c.txt"
+    syn.write_text(str(corpus))
+    out, rep = tmp_path / "v.txt", tmp_path / "r.txt"
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        "-m", "paper_1604_04661_b200", "train-dist", "-train", str(corpus),
+                        "-output", str(out), "-size", "16", "-iter", "2", "-min-count", "1",
+                        "-sync-period", "20000", "-report", str(rep)],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    items = dict(line.split(": ", 1) for line in rep.read_text().splitlines())
+    assert items["command"] == "train-dist" and items["transport"] == "nccl" and items["nodes"] == "1"
+    assert int(items["words_read"]) == 2 * syn.encoded.n_tokens
+    from paper_1604_04661_b200.model import load_model
+    m, v = load_model(str(out))
+    assert m.input_vectors.shape == (syn.vocab.size, 16) and np.isfinite(m.input_vectors).all()
