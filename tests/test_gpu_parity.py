@@ -372,25 +372,29 @@ def test_fast_driver_windows_match_oracle(workers):
     assert run.words_trained == orc.workers[0].words_trained
 
 
-def test_fast_driver_single_worker_trains_like_oracle():
+@pytest.mark.parametrize("D,k", [(64, 5), (300, 7), (512, 2), (100, 3), (320, 5), (4, 6)])
+def test_fast_driver_single_worker_trains_like_oracle(D, k):
     """One worker, dynamic schedule: same windows in the same order -> fp32 model within
-    accumulated rounding of the oracle's float64-accumulating restatement; loss within 1e-3."""
+    accumulated rounding of the oracle's float64-accumulating restatement; loss within 1e-3.
+    Covers the fast kernel's variants: exact K1 = 6 and padded K1R = 8, whole-slot rows
+    (d = 64, 320, 512) and partial last slots (d = 4, 100, 300)."""
     P = _pkg()
     from paper_1604_04661_b200.synthetic import make_planted_corpus
     from paper_1604_04661_b200.model import DeviceModel
     O = _oracle()
     syn = make_planted_corpus(30_000, 400, n_clusters=4, cluster_size=5, sentence_len=37, seed=7)
     ids, off, counts = syn.encoded.ids, syn.encoded.offsets, syn.vocab.counts
-    V, D = len(counts), 64
+    V = len(counts)
     base = O.init_model(V, D, 3).astype(np.float32)
     dm = DeviceModel.from_host(P.EmbeddingModel(base.copy(), np.zeros_like(base)))
-    run, sampler = _run_driver(ids, off, counts, window=5, k=5, cap=16, dynamic=True, subsample=1e-3,
+    run, sampler = _run_driver(ids, off, counts, window=5, k=k, cap=16, dynamic=True, subsample=1e-3,
                                seed=9, stream_base=0, table_len=None, rng="philox", workers=1,
                                epochs=2, update=True, model=dm, dim=D, loss_every=3, trace_cap=0,
                                schedule="dynamic")
+    assert run.dynamic
     m_in, m_out = base.copy(), np.zeros_like(base)
     orc = _oracle_philox(ids, off, counts, sampler.host_alias, W=1, epochs=2, update=True,
-                         m_in=m_in, m_out=m_out, loss_every=3)
+                         m_in=m_in, m_out=m_out, loss_every=3, k=k)
     got = dm.to_host()
     np.testing.assert_allclose(run.loss_by_epoch(), orc.stats()[2], rtol=1e-3)
     assert np.abs(got.input_vectors - m_in).max() < 1e-3 * np.abs(m_in).max()
