@@ -58,7 +58,7 @@ struct FastArgs {
 };
 
 struct FastSlab {
-  int64_t rows, e, ids, roff, kept, koff, bw, total;
+  int64_t rows, e, ids, roff, kept, koff, bw, cnt, total;
 };
 __host__ __device__ inline FastSlab fast_slab(int64_t ld, int mcap, int k1r, int kept_cap) {
   FastSlab s;
@@ -70,7 +70,8 @@ __host__ __device__ inline FastSlab fast_slab(int64_t ld, int mcap, int k1r, int
   s.kept = s.roff + round16_(int64_t(2) * idsn * 4);
   s.koff = s.kept + round16_(int64_t(kept_cap) * 4);
   s.bw = s.koff + round16_(int64_t(kept_cap) * 4);
-  s.total = s.bw + round16_(int64_t(kept_cap) * 4);
+  s.cnt = s.bw + round16_(int64_t(kept_cap) * 4);  // 6 x 8-byte counters, lane 0 only
+  s.total = s.cnt + 48;
   return s;
 }
 
@@ -183,6 +184,28 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
   int *kept_s = reinterpret_cast<int *>(base + L.kept);
   int *koff_s = reinterpret_cast<int *>(base + L.koff);
   int *bw_s = reinterpret_cast<int *>(base + L.bw);
+  // words trained / read, chunks, inputs, and the current epoch's sampled loss cells and
+  // loss sum of this worker: kept in shared memory (lane 0) rather than in 64-bit
+  // registers live across the whole hot loop
+  long long *cnt_s = reinterpret_cast<long long *>(base + L.cnt);
+  double *loss_s = reinterpret_cast<double *>(cnt_s + 5);
+  if (lane == 0) {
+    cnt_s[0] = cnt_s[1] = cnt_s[2] = cnt_s[3] = cnt_s[4] = 0;
+    *loss_s = 0.0;
+  }
+  // lane 0: move the current epoch's loss into the per-epoch and per-launch totals
+  auto flush_epoch_loss = [&](int e) {
+    if (lane == 0) {
+      p.loss_by_epoch[(int64_t)wid * p.epochs + e] += *loss_s;
+      p.cells_by_epoch[(int64_t)wid * p.epochs + e] += cnt_s[4];
+      if (p.totals != nullptr) {
+        atomicAdd(p.totals + 4, (unsigned long long)cnt_s[4]);
+        atomicAdd(p.loss_total, *loss_s);
+      }
+      *loss_s = 0.0;
+      cnt_s[4] = 0;
+    }
+  };
   const int idsn = mcap + K1R;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int ld = (int)p.mv.ld;  // shared-memory indexing in 32 bits
@@ -200,9 +223,6 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
   const int64_t shard_tokens = p.offsets[p.shard_lo + p.n_sent] - off0;
   const int rec_len = 4 + p.cap + k1;
 
-  long long chunks = 0, trained = 0, inputs = 0, read = 0;
-  double loss = 0.0;
-  long long cells = 0;
   int loss_epoch = -1;
 
   for (;;) {
@@ -219,7 +239,7 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
       continue;
     }
     const uint32_t ep = p.epoch_base + (uint32_t)epoch;
-    read += n;
+    if (lane == 0) cnt_s[1] += n;
     // alpha from the sentence's words-read position (update_alpha, trainer.py:122-132)
     const double pos_words = (double)(p.words_base + (int64_t)epoch * shard_tokens + (lo_t - off0));
     double frac = 1.0 - pos_words / (p.total_x_epochs + 1.0);
@@ -227,21 +247,7 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
     const float alpha = (float)(p.alpha0 * frac);
     const bool want = p.loss_every > 0 && ((int64_t)c % p.loss_every) == 0;
     if (want && epoch != loss_epoch) {
-      if (loss_epoch >= 0) {
-        double l2 = loss;
-        long long c2 = cells;
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) {
-          l2 += __shfl_xor_sync(0xffffffffu, l2, o);
-          c2 += __shfl_xor_sync(0xffffffffu, c2, o);
-        }
-        if (lane == 0) {
-          p.loss_by_epoch[(int64_t)wid * p.epochs + loss_epoch] += l2;
-          p.cells_by_epoch[(int64_t)wid * p.epochs + loss_epoch] += c2;
-        }
-        loss = 0.0;
-        cells = 0;
-      }
+      if (loss_epoch >= 0) flush_epoch_loss(loss_epoch);
       loss_epoch = epoch;
     }
     // subsample: one Philox uniform per token, survivors compacted in order
@@ -274,7 +280,7 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
       bw_s[q] = b;
     }
     __syncwarp();
-    trained += nk;
+    if (lane == 0) cnt_s[0] += nk;
 
     Unit u;
     if (!first_unit(bw_s, nk, p.cap, u)) continue;
@@ -331,8 +337,10 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
         tok_n = (uint64_t)(p.token_base + lo_t + koff_s[nx.pos]);
         if (lane < min(32, p.k_neg + 2)) cand_n = neg_candidate(p, tok_n, ep, nx.ch, lane);
       }
-      chunks += 1;
-      inputs += m;
+      if (lane == 0) {
+        cnt_s[2] += 1;
+        cnt_s[3] += m;
+      }
       if (p.trace_cap > 0) {
         unsigned long long idx = 0;
         if (lane == 0) idx = atomicAdd(p.trace_count, 1ULL);
@@ -389,9 +397,16 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
         const bool live = kk < k1 && (hk == 0 || two);
         cell_error_f32(sc, kk, alpha, sig_s, er, es);
         if (live) e_s[(i + hk) * 8 + kk] = es;  // both lanes of the pair hold the same value
-        if (want && live && (lane & 1) == 0) {
-          loss += softplus(kk == 0 ? -(double)sc : (double)sc);
-          cells += 1;
+        if (want) {  // sampled sentence: warp-reduce this pair's softplus terms
+          const bool mine = live && (lane & 1) == 0;
+          double sp = mine ? softplus(kk == 0 ? -(double)sc : (double)sc) : 0.0;
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
+          const int nc = __popc(__ballot_sync(0xffffffffu, mine));
+          if (lane == 0) {
+            *loss_s += sp;
+            cnt_s[4] += nc;
+          }
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -487,26 +502,14 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
     }
   }
   // flush this worker's counters
-  if (loss_epoch >= 0) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      loss += __shfl_xor_sync(0xffffffffu, loss, o);
-      cells += __shfl_xor_sync(0xffffffffu, cells, o);
-    }
-    if (lane == 0) {
-      p.loss_by_epoch[(int64_t)wid * p.epochs + loss_epoch] += loss;
-      p.cells_by_epoch[(int64_t)wid * p.epochs + loss_epoch] += cells;
-    }
-  }
+  if (loss_epoch >= 0) flush_epoch_loss(loss_epoch);
+  __syncwarp();
+  const long long trained = cnt_s[0], read = cnt_s[1], chunks = cnt_s[2], inputs = cnt_s[3];
   if (lane == 0 && p.totals != nullptr) {
     atomicAdd(p.totals + 0, (unsigned long long)trained);
     atomicAdd(p.totals + 1, (unsigned long long)read);
     atomicAdd(p.totals + 2, (unsigned long long)chunks);
     atomicAdd(p.totals + 3, (unsigned long long)inputs);
-    if (loss_epoch >= 0) {
-      atomicAdd(p.totals + 4, (unsigned long long)cells);
-      atomicAdd(p.loss_total, loss);
-    }
   }
   if (lane == 0) {
     sgns_worker &o = p.workers[wid];
