@@ -219,8 +219,6 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
   auto slot_ok = [&](int j) { return FULL || j < NS - 1 || lane + 32 * j < nslot; };
   auto chunk_ok = [&](int j) { return j < NCH - 1 || lane + 32 * j < nvec; };
   auto kk_ok = [&](int k) { return EXACT_K || k < k1; };
-  const int64_t off0 = p.offsets[p.shard_lo];
-  const int64_t shard_tokens = p.offsets[p.shard_lo + p.n_sent] - off0;
   const int rec_len = 4 + p.cap + k1;
 
   int loss_epoch = -1;
@@ -241,6 +239,10 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
     const uint32_t ep = p.epoch_base + (uint32_t)epoch;
     if (lane == 0) cnt_s[1] += n;
     // alpha from the sentence's words-read position (update_alpha, trainer.py:122-132)
+    // (the shard's bounds are re-read per sentence -- two cached loads -- rather than
+    // held in four registers across the hot loop)
+    const int64_t off0 = __ldg(p.offsets + p.shard_lo);
+    const int64_t shard_tokens = __ldg(p.offsets + p.shard_lo + p.n_sent) - off0;
     const double pos_words = (double)(p.words_base + (int64_t)epoch * shard_tokens + (lo_t - off0));
     double frac = 1.0 - pos_words / (p.total_x_epochs + 1.0);
     if (frac < p.floor_frac) frac = p.floor_frac;
@@ -455,12 +457,9 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
       }
       __syncwarp();
       // dC_k = sum_i (alpha err_ik) A_i, column-outer; patch u+1's prefetched copies.
-      // Row base pointers (lane offset folded in) are formed once, so every scatter
-      // below addresses [row + 256 j] with an immediate offset.
-      float *orow[K1R];
+      uint32_t orow[K1R];  // 32-bit row offsets: one IMAD.WIDE per scatter, 6 registers
 #pragma unroll
-      for (int k = 0; k < K1R; ++k)
-        orow[k] = out_dst_l + off_s[m + (kk_ok(k) ? k : 0)];
+      for (int k = 0; k < K1R; ++k) orow[k] = off_s[m + (kk_ok(k) ? k : 0)];
 #pragma unroll
       for (int j = 0; j < NS; ++j) {
         if (!slot_ok(j)) continue;
@@ -481,7 +480,7 @@ __global__ void __maxnreg__(SGNS_FAST_MAXNREG) drive_fast_kernel(FastArgs p) {
         }
 #pragma unroll
         for (int k = 0; k < K1R; ++k)
-          if (kk_ok(k)) atomicAdd(reinterpret_cast<float2 *>(orow[k] + 64 * j), acc[k]);
+          if (kk_ok(k)) atomicAdd(reinterpret_cast<float2 *>(out_dst_l + orow[k] + 64 * j), acc[k]);
         if (lo_bits | hi_bits) {
 #pragma unroll
           for (int k = 0; k < K1R; ++k) {
