@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--micro-ids", choices=["zipf", "uniform"], default="zipf",
                     help="--config micro: id distribution (uniform = no hot rows, diagnostic)")
+    ap.add_argument("--micro-shape", default="",
+                    help="--config micro: run only shapes matching 'n_win,d,w,K[,dyn]' (e.g. 65536,300,5,5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--sync-hot-rows", type=int, default=-1,
@@ -300,13 +302,16 @@ def micro_bench(args):
               (65536, 300, 10, 5, False), (65536, 300, 5, 10, False), (65536, 300, 5, 15, False),
               (65536, 100, 10, 15, False), (65536, 300, 5, 5, True)]
     T = len(os.sched_getaffinity(0))
-    rng = np.random.default_rng(args.seed)
     ranks = np.arange(1, V + 1, dtype=np.float64)
     pz = 1.0 / ranks if args.micro_ids == "zipf" else np.ones_like(ranks)
     pz /= pz.sum()
     pn = pz ** 0.75
     pn /= pn.sum()
+    if args.micro_shape:
+        want = [int(x) for x in args.micro_shape.split(",")]
+        shapes = [sh for sh in shapes if list(sh[:4]) == want[:4] and (len(want) < 5 or int(sh[4]) == want[4])]
     for n_win, d, w, k, dyn in shapes:
+        rng = np.random.default_rng([args.seed, n_win, d, w, k, int(dyn)])  # per shape: filterable
         sig = d ** -0.25
         base_in = (rng.normal(size=(V, d)) * sig).astype(np.float32)
         base_out = (rng.normal(size=(V, d)) * sig).astype(np.float32)
