@@ -375,12 +375,20 @@ __device__ __forceinline__ void f2_load_c(float2 (&c)[K1R][NS], const ModelView<
   }
 }
 
-template <int NS, int NCH, int K1R, bool EXACT_K>
+// HOT (snapshot mode only): dA of row 0 -- the most frequent word in the reference's
+// count-sorted vocabulary (corpus.py:86-105), about 8% of all input slots under Zipf --
+// is summed into the warp's register accumulator `hot` instead of being scattered, and
+// the caller adds it to the model once per warp.  Each window's delta is rounded as in
+// the scatter path; only the summation order changes, which the concurrent scatters leave
+// unspecified anyway.  Without it every window's row-0 dA queues on the same few L2
+// lines (per-address serialised red.add).
+template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT>
 __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const ModelView<float> &mv,
                                             const F2Shape<NS, NCH> &sh, const uint32_t *off_s,
                                             int m, int k1, float alpha, bool exact,
                                             const float *sig_s, bool want_loss, double &loss_acc,
-                                            long long &cell_acc, const float *rows_s, float *e_s) {
+                                            long long &cell_acc, const float *rows_s, float *e_s,
+                                            float2 (&hot)[NS]) {
   constexpr int NV = 8;
   static_assert(K1R <= NV, "K1R <= 8");
   const int lane = sh.lane;
@@ -438,10 +446,16 @@ __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const Mo
 #pragma unroll
         for (int j = 0; j < NS; ++j) d[j] = k == 0 ? __fmul2_rn(ek2, c[0][j]) : __ffma2_rn(ek2, c[k][j], d[j]);
       }
-      float *dst = in_dst_l + off_s[i + h];
+      const uint32_t ro = off_s[i + h];
+      if (HOT && ro == 0) {
 #pragma unroll
-      for (int j = 0; j < NS; ++j)
-        if (sh.slot_ok(j)) atomicAdd(reinterpret_cast<float2 *>(dst + 64 * j), __fmul2_rn(d[j], alpha2));
+        for (int j = 0; j < NS; ++j) hot[j] = __fadd2_rn(hot[j], __fmul2_rn(d[j], alpha2));
+      } else {
+        float *dst = in_dst_l + ro;
+#pragma unroll
+        for (int j = 0; j < NS; ++j)
+          if (sh.slot_ok(j)) atomicAdd(reinterpret_cast<float2 *>(dst + 64 * j), __fmul2_rn(d[j], alpha2));
+      }
     }
   }
   __syncwarp();
@@ -478,19 +492,20 @@ __device__ __forceinline__ void f2_dc(const ModelView<float> &mv, const F2Shape<
   __syncwarp();
 }
 
-template <int NS, int NCH, int K1R, bool EXACT_K>
+template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT = false>
 __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, const uint32_t *off_s,
                                                  int m, int k1, float alpha, bool exact,
                                                  const float *sig_s, bool want_loss,
                                                  double &loss_acc, long long &cell_acc,
-                                                 float *rows_s, float *e_s, int lane) {
+                                                 float *rows_s, float *e_s, int lane,
+                                                 float2 (&hot)[NS]) {
   if constexpr (EXACT_K) k1 = K1R;
   const F2Shape<NS, NCH> sh(mv, lane);
   f2_issue_a<NS, NCH>(mv, sh, off_s, m, rows_s);
   float2 c[K1R][NS];
   f2_load_c<NS, NCH, K1R, EXACT_K>(c, mv, sh, off_s + m, k1);
-  f2_score_da<NS, NCH, K1R, EXACT_K>(c, mv, sh, off_s, m, k1, alpha, exact, sig_s, want_loss, loss_acc,
-                                     cell_acc, rows_s, e_s);
+  f2_score_da<NS, NCH, K1R, EXACT_K, HOT>(c, mv, sh, off_s, m, k1, alpha, exact, sig_s, want_loss,
+                                          loss_acc, cell_acc, rows_s, e_s, hot);
   f2_dc<NS, NCH, K1R, EXACT_K>(mv, sh, off_s, m, k1, rows_s, e_s);
 }
 
@@ -500,12 +515,13 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
 // shared by a pair of inputs; one transposed butterfly over 32 values reduces both
 // inputs' scores; error rows are padded to 16 floats.  rows_s holds the m input rows
 // then the k1 output rows.
-template <int NS, int NCH>
+template <int NS, int NCH, bool HOT = false>
 __device__ __forceinline__ void window_update_f2s(const ModelView<float> &mv, const uint32_t *off_s,
                                                   int m, int k1, float alpha, bool exact,
                                                   const float *sig_s, bool want_loss,
                                                   double &loss_acc, long long &cell_acc,
-                                                  float *rows_s, float *e_s, int lane) {
+                                                  float *rows_s, float *e_s, int lane,
+                                                  float2 (&hot)[NS]) {
   constexpr int KM = 16;
   const int64_t ld = mv.ld;
   const int nvec = mv.nvec, nslot = nvec * 2;
@@ -578,14 +594,20 @@ __device__ __forceinline__ void window_update_f2s(const ModelView<float> &mv, co
         d1[j] = __ffma2_rn(make_float2(e1, e1), c, d1[j]);
       }
     }
+    // HOT: row 0's dA goes to the warp's register accumulator (see f2_score_da)
+    const bool hot0 = HOT && off_s[i] == 0, hot1 = HOT && two && off_s[i1] == 0;
     float *dst0 = mv.in_dst + off_s[i] + 2 * lane;
     float *dst1 = mv.in_dst + off_s[i1] + 2 * lane;
 #pragma unroll
-    for (int j = 0; j < NS; ++j)
+    for (int j = 0; j < NS; ++j) {
+      const float2 u0 = __fmul2_rn(d0[j], alpha2), u1 = __fmul2_rn(d1[j], alpha2);
+      if (hot0) hot[j] = __fadd2_rn(hot[j], u0);
+      if (hot1) hot[j] = __fadd2_rn(hot[j], u1);
       if (slot_ok(j)) {
-        atomicAdd(reinterpret_cast<float2 *>(dst0 + 64 * j), __fmul2_rn(d0[j], alpha2));
-        if (two) atomicAdd(reinterpret_cast<float2 *>(dst1 + 64 * j), __fmul2_rn(d1[j], alpha2));
+        if (!hot0) atomicAdd(reinterpret_cast<float2 *>(dst0 + 64 * j), u0);
+        if (two && !hot1) atomicAdd(reinterpret_cast<float2 *>(dst1 + 64 * j), u1);
       }
+    }
   }
   __syncwarp();
   // dC_k = sum_i (alpha err_ik) A_i, column-outer, outputs in groups of 8

@@ -18,6 +18,15 @@
 #include "sgns_device.cuh"
 #include "sgns_fast.cuh"
 
+// The library is built from this one file as four translation units compiled in parallel
+// (SGNS_PART 0: C ABI + init/slot kernels, 1: update_windows, 2: static driver, 3: fast
+// driver; see __graft_entry__.build_lib).  Without SGNS_PART it is a single unit.
+#ifdef SGNS_PART
+#define SGNS_HAS(n) (SGNS_PART == (n))
+#else
+#define SGNS_HAS(n) 1
+#endif
+
 namespace sgns {
 
 constexpr int kMaxSentence = 1024;
@@ -73,21 +82,24 @@ __device__ __forceinline__ void flush_loss(double loss, long long cells, double 
 
 // K1R == 6 is instantiated for k1 == 6 exactly (K = 5, the north-star shape); K1R == 8
 // covers k1 <= 8 with predicates.
-template <typename T, int MODE, int NS, int NCH, int K1R>
+// HOT: see f2_score_da (float32 k1 <= 16 paths, snapshot mode); `hot` is the warp's row-0
+// dA accumulator, unused otherwise.
+__host__ __device__ constexpr int hot_slots(int ns) { return ns > 0 ? ns : 1; }
+template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT = false>
 __device__ __forceinline__ void run_window(const ModelView<T> &mv, const int *ids_s, uint32_t *roff_s,
                                            int m, int k1, T alpha, bool exact, const T *sig_s,
                                            bool want, double &loss, long long &cells, T *rows_s,
-                                           T *e_s, int lane) {
+                                           T *e_s, int lane, float2 (&hot)[hot_slots(NS)]) {
   if constexpr (MODE == MODE_F2) {
     for (int r = lane; r < m + k1; r += 32) roff_s[r] = (uint32_t)ids_s[r] * (uint32_t)mv.ld;
     __syncwarp();
-    window_update_f2<NS, NCH, K1R, K1R == 6>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss,
-                                             cells, rows_s, e_s, lane);
+    window_update_f2<NS, NCH, K1R, K1R == 6, HOT>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss,
+                                                  cells, rows_s, e_s, lane, hot);
   } else if constexpr (MODE == MODE_F2S) {
     for (int r = lane; r < m + k1; r += 32) roff_s[r] = (uint32_t)ids_s[r] * (uint32_t)mv.ld;
     __syncwarp();
-    window_update_f2s<NS, NCH>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss, cells, rows_s,
-                               e_s, lane);
+    window_update_f2s<NS, NCH, HOT>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss, cells,
+                                    rows_s, e_s, lane, hot);
   } else {
     window_update<T, NCH>(mv, ids_s, m, k1, alpha, exact, sig_s, want, loss, cells,
                                     rows_s, e_s, lane);
@@ -108,7 +120,7 @@ template <typename T> struct UpdateArgs {
   int wpb;
 };
 
-template <typename T, int MODE, int NS, int NCH, int K1R>
+template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT>
 __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) update_windows_kernel(UpdateArgs<T> p) {
   extern __shared__ __align__(16) unsigned char smem[];
   T *sig_s = reinterpret_cast<T *>(smem);
@@ -122,7 +134,11 @@ __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) update_windows
   uint32_t *roff_s = reinterpret_cast<uint32_t *>(base + L.roff);
   double loss = 0.0;
   long long cells = 0;
-  for (int w = blockIdx.x * p.wpb + warp; w < p.n_win; w += gridDim.x * p.wpb) {
+  float2 hot[hot_slots(NS)];
+#pragma unroll
+  for (int j = 0; j < hot_slots(NS); ++j) hot[j] = make_float2(0.f, 0.f);
+  const int step = gridDim.x * p.wpb;
+  for (int w = blockIdx.x * p.wpb + warp; w < p.n_win; w += step) {
     const int lo = p.in_off[w], hi = p.in_off[w + 1];
     const int m = hi - lo;
     if (m < 1 || m > p.mcap) {
@@ -133,8 +149,22 @@ __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) update_windows
       ids_s[r] = r < m ? p.in_ids[lo + r] : p.out_ids[(int64_t)w * p.k1 + (r - m)];
     __syncwarp();
     const bool want = p.loss_every > 0 && (w % p.loss_every) == 0;
-    run_window<T, MODE, NS, NCH, K1R>(p.mv, ids_s, roff_s, m, p.k1, p.alpha[w], p.exact != 0, sig_s,
-                                      want, loss, cells, rows_s, e_s, lane);
+    run_window<T, MODE, NS, NCH, K1R, HOT>(p.mv, ids_s, roff_s, m, p.k1, p.alpha[w], p.exact != 0,
+                                           sig_s, want, loss, cells, rows_s, e_s, lane, hot);
+  }
+
+  if constexpr (HOT && (MODE == MODE_F2 || MODE == MODE_F2S)) {
+    // the warp's accumulated row-0 dA: one scatter per warp, none when row 0 never occurred
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) any |= hot[j].x != 0.f || hot[j].y != 0.f;
+    if (__any_sync(0xffffffffu, any)) {
+      float *dst = reinterpret_cast<float *>(p.mv.in_dst) + 2 * lane;
+#pragma unroll
+      for (int j = 0; j < NS; ++j)
+        if (j < NS - 1 || lane + 32 * j < 2 * p.mv.nvec)
+          atomicAdd(reinterpret_cast<float2 *>(dst + 64 * j), hot[j]);
+    }
   }
   if (p.loss_every > 0) flush_loss<T>(loss, cells, p.loss_sum, p.loss_cells, true, lane);
 }
@@ -394,9 +424,11 @@ __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) drive_kernel(D
           __syncwarp();
           if (lane == 0) p.trace_count[wid] = idx + 1;
         }
-        if (p.update)
+        if (p.update) {
+          float2 no_hot[hot_slots(NS)];  // in-place training: no deferred rows
           run_window<T, MODE, NS, NCH, K1R>(p.mv, ids_s, roff_s, mc, k1, alpha_t, p.exact != 0, sig_s,
-                                            want, loss, cells, rows_s, e_s, lane);
+                                            want, loss, cells, rows_s, e_s, lane, no_hot);
+        }
         __syncwarp();
       }
       if (RNG == SGNS_RNG_SPLITMIX) rng = sb.state_after();
@@ -426,6 +458,7 @@ __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) drive_kernel(D
   }
 }
 
+#if SGNS_HAS(0)
 // ------------------------------------------------------------------ init ----
 template <typename T>
 __global__ void init_model_kernel(T *m_in, T *m_out, int64_t V, int dim, int64_t ld, uint64_t s0) {
@@ -458,6 +491,8 @@ __global__ void expand_slots_kernel(const int64_t *bounds, int64_t V, int32_t *s
     slots[sidx] = (int32_t)lo;
   }
 }
+
+#endif  // SGNS_HAS(0)
 
 // ----------------------------------------------------------- dispatching ----
 static int nch_for(int nvec) {
@@ -512,9 +547,19 @@ static int choose_wpb(K kernel, int64_t table, int64_t slab, int *wpb_out, int *
   return 0;
 }
 
-template <typename T, int MODE, int NS, int NCH, int K1R>
+// entry points of the parts (defined in parts 1, 2, 3)
+int update_f32(UpdateArgs<float> a, cudaStream_t st);
+int update_f64(UpdateArgs<double> a, cudaStream_t st);
+int drive_static(const sgns_drive_params *p, cudaStream_t st, int *resident);
+int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident);
+
+static int ns_for(int64_t ld_elems_f32) { return (int)((ld_elems_f32 / 2 + 31) / 32); }
+static bool offsets32_ok(int64_t vocab, int64_t ld) { return vocab * ld < (int64_t(1) << 32); }
+
+#if SGNS_HAS(1)
+template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT = false>
 static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
-  auto kern = update_windows_kernel<T, MODE, NS, NCH, K1R>;
+  auto kern = update_windows_kernel<T, MODE, NS, NCH, K1R, HOT>;
   const Slab L = slab_layout(MODE, sizeof(T), a.mv.ld, a.mcap, a.k1, 0);
   int wpb = 0, bps = 0;
   int rc = choose_wpb(kern, table_bytes(sizeof(T)), L.total, &wpb, &bps);
@@ -528,6 +573,9 @@ static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
   return (int)cudaGetLastError();
 }
 
+#endif  // SGNS_HAS(1)
+
+#if SGNS_HAS(2)
 template <typename T, int MODE, int NS, int NCH, int K1R, int RNG>
 static int launch_drive_t(DriveArgs<T> a, int wpb_req, cudaStream_t st, int *resident = nullptr) {
   auto kern = drive_kernel<T, MODE, NS, NCH, K1R, RNG>;
@@ -550,8 +598,6 @@ static int launch_drive_t(DriveArgs<T> a, int wpb_req, cudaStream_t st, int *res
 }
 
 // float32 fast path: k1 <= 8, d <= 512 (NS = float2 slots per lane), V * ld < 2^32
-static int ns_for(int64_t ld_elems_f32) { return (int)((ld_elems_f32 / 2 + 31) / 32); }
-static bool offsets32_ok(int64_t vocab, int64_t ld) { return vocab * ld < (int64_t(1) << 32); }
 
 template <int NS, int RNG>
 static int drive_f2(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
@@ -614,19 +660,29 @@ static int drive_f64(DriveArgs<double> a, int wpb, cudaStream_t st, int *res) {
   return SGNS_E_SHAPE;
 }
 
+#endif  // SGNS_HAS(2)
+
+#if SGNS_HAS(1)
 template <int NS>
 static int update_f2(UpdateArgs<float> a, cudaStream_t st) {
   constexpr int NCH = (NS + 1) / 2;
-  if (a.k1 == 6) return launch_update_t<float, MODE_F2, NS, NCH, 6>(a, st);
-  return launch_update_t<float, MODE_F2, NS, NCH, 8>(a, st);
+  // snapshot mode (rows gathered from a separate source): row 0's dA is combined per warp
+  const bool hot = static_cast<const float *>(a.mv.in_dst) != a.mv.in_src;
+  if (a.k1 == 6)
+    return hot ? launch_update_t<float, MODE_F2, NS, NCH, 6, true>(a, st)
+               : launch_update_t<float, MODE_F2, NS, NCH, 6, false>(a, st);
+  return hot ? launch_update_t<float, MODE_F2, NS, NCH, 8, true>(a, st)
+             : launch_update_t<float, MODE_F2, NS, NCH, 8, false>(a, st);
 }
 
 template <int NS>
 static int update_f2s(UpdateArgs<float> a, cudaStream_t st) {
-  return launch_update_t<float, MODE_F2S, NS, (NS + 1) / 2, 16>(a, st);
+  const bool hot = static_cast<const float *>(a.mv.in_dst) != a.mv.in_src;  // snapshot mode
+  return hot ? launch_update_t<float, MODE_F2S, NS, (NS + 1) / 2, 16, true>(a, st)
+             : launch_update_t<float, MODE_F2S, NS, (NS + 1) / 2, 16, false>(a, st);
 }
 
-static int update_f32(UpdateArgs<float> a, cudaStream_t st) {
+int update_f32(UpdateArgs<float> a, cudaStream_t st) {
   const int ns = ns_for(a.mv.ld);
   if (a.k1 > 8 && a.k1 <= 16 && offsets32_ok(a.vocab, a.mv.ld)) {
     switch (ns) {
@@ -662,7 +718,7 @@ static int update_f32(UpdateArgs<float> a, cudaStream_t st) {
   return SGNS_E_SHAPE;
 }
 
-static int update_f64(UpdateArgs<double> a, cudaStream_t st) {
+int update_f64(UpdateArgs<double> a, cudaStream_t st) {
   switch (nch_for(a.mv.nvec)) {
     case 1: return launch_update_t<double, MODE_SMEM, 0, 1, 0>(a, st);
     case 2: return launch_update_t<double, MODE_SMEM, 0, 2, 0>(a, st);
@@ -673,6 +729,9 @@ static int update_f64(UpdateArgs<double> a, cudaStream_t st) {
   return SGNS_E_SHAPE;
 }
 
+#endif  // SGNS_HAS(1)
+
+#if SGNS_HAS(2)
 template <typename T>
 static void fill_drive_args(DriveArgs<T> &a, const sgns_drive_params *p) {
   std::memset(&a, 0, sizeof(a));
@@ -717,6 +776,24 @@ static void fill_drive_args(DriveArgs<T> &a, const sgns_drive_params *p) {
   a.epoch_base = (uint32_t)p->epoch_base;
 }
 
+int drive_static(const sgns_drive_params *p, cudaStream_t st, int *resident) {
+  const int wpb = p->warps_per_block;
+  if (p->dtype == SGNS_F32) {
+    DriveArgs<float> a;
+    fill_drive_args(a, p);
+    if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
+    return p->rng_mode == SGNS_RNG_SPLITMIX ? drive_f32<SGNS_RNG_SPLITMIX>(a, wpb, st, resident)
+                                            : drive_f32<SGNS_RNG_PHILOX>(a, wpb, st, resident);
+  }
+  DriveArgs<double> a;
+  fill_drive_args(a, p);
+  if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
+  return p->rng_mode == SGNS_RNG_SPLITMIX ? drive_f64<SGNS_RNG_SPLITMIX>(a, wpb, st, resident)
+                                          : drive_f64<SGNS_RNG_PHILOX>(a, wpb, st, resident);
+}
+#endif  // SGNS_HAS(2)
+
+#if SGNS_HAS(3)
 // ------------------------------------------------------------ fast path ----
 template <int NS, int K1R, bool EXACT, bool FULL>
 static int launch_fast_t(FastArgs a, int wpb_req, cudaStream_t st, int *resident) {
@@ -749,14 +826,7 @@ static int fast_ns(FastArgs a, int wpb, cudaStream_t st, int *res) {
               : launch_fast_t<NS, 8, false, false>(a, wpb, st, res);
 }
 
-static bool fast_eligible(const sgns_drive_params *p) {
-  const int64_t ld = p->ld;
-  return p->dtype == SGNS_F32 && p->rng_mode == SGNS_RNG_PHILOX && p->k_neg + 1 <= 8 &&
-         ns_for(ld) >= 1 && ns_for(ld) <= 8 && offsets32_ok(p->vocab, ld) &&
-         p->sigmoid_mode == SGNS_SIGMOID_TABLE;
-}
-
-static int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
+int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
   FastArgs a;
   std::memset(&a, 0, sizeof(a));
   float *mi = static_cast<float *>(p->d_m_in), *mo = static_cast<float *>(p->d_m_out);
@@ -812,24 +882,22 @@ static int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resid
   return SGNS_E_SHAPE;
 }
 
+#endif  // SGNS_HAS(3)
+
+#if SGNS_HAS(0)
+static bool fast_eligible(const sgns_drive_params *p) {
+  const int64_t ld = p->ld;
+  return p->dtype == SGNS_F32 && p->rng_mode == SGNS_RNG_PHILOX && p->k_neg + 1 <= 8 &&
+         ns_for(ld) >= 1 && ns_for(ld) <= 8 && offsets32_ok(p->vocab, ld) &&
+         p->sigmoid_mode == SGNS_SIGMOID_TABLE;
+}
+
 static int drive_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
   if (p->schedule == SGNS_SCHEDULE_DYNAMIC) {
     if (!fast_eligible(p)) return SGNS_E_ARG;
     return fast_dispatch(p, st, resident);
   }
-  const int wpb = p->warps_per_block;
-  if (p->dtype == SGNS_F32) {
-    DriveArgs<float> a;
-    fill_drive_args(a, p);
-    if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
-    return p->rng_mode == SGNS_RNG_SPLITMIX ? drive_f32<SGNS_RNG_SPLITMIX>(a, wpb, st, resident)
-                                            : drive_f32<SGNS_RNG_PHILOX>(a, wpb, st, resident);
-  }
-  DriveArgs<double> a;
-  fill_drive_args(a, p);
-  if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
-  return p->rng_mode == SGNS_RNG_SPLITMIX ? drive_f64<SGNS_RNG_SPLITMIX>(a, wpb, st, resident)
-                                          : drive_f64<SGNS_RNG_PHILOX>(a, wpb, st, resident);
+  return drive_static(p, st, resident);
 }
 
 static bool ld_ok(int32_t dtype, int32_t dim, int64_t ld) {
@@ -837,9 +905,13 @@ static bool ld_ok(int32_t dtype, int32_t dim, int64_t ld) {
   return dim >= 1 && ld >= dim && (ld * elem) % 16 == 0;
 }
 
+#endif  // SGNS_HAS(0)
+
 }  // namespace sgns
 
 using namespace sgns;
+
+#if SGNS_HAS(0)
 
 extern "C" {
 
@@ -1030,3 +1102,5 @@ int sgns_build_alias(const int64_t *h_counts, int64_t vocab, double power, uint3
 }
 
 }  // extern "C"
+
+#endif  // SGNS_HAS(0)

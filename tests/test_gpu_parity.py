@@ -178,7 +178,8 @@ def test_disjoint_windows_equal_sequential(dtype, D, k):
                                        ("f32", 64, 7)])
 def test_snapshot_conflicting_windows(dtype, D, k):
     """P3: Zipf-conflicting windows in snapshot mode == snapshot + sum of per-window deltas
-    (float32: the hottest rows' adds are combined in shared memory per CTA first)."""
+    (float32 snapshot mode sums row 0's dA per warp in registers before one scatter; Zipf(1.3)
+    puts id 0 in ~30% of the slots here)."""
     P, O = _pkg(), _oracle()
     from paper_1604_04661_b200.kernel_batched import DeviceWindowBatch, WindowBatch
     from paper_1604_04661_b200.model import DeviceModel, SIGMOID_TABLE_F32, SIGMOID_TABLE_F64
