@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--micro-ids", choices=["zipf", "uniform"], default="zipf",
                     help="--config micro: id distribution (uniform = no hot rows, diagnostic)")
     ap.add_argument("--micro-shape", default="",
-                    help="--config micro: run only shapes matching 'n_win,d,w,K[,dyn]' (e.g. 65536,300,5,5)")
+                    help="--config micro: run only shapes matching 'n_win,d,w,K[,dyn]' (e.g. 65536,300,5,5), ';'-separated, in that order")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--sync-hot-rows", type=int, default=-1,
@@ -308,8 +308,11 @@ def micro_bench(args):
     pn = pz ** 0.75
     pn /= pn.sum()
     if args.micro_shape:
-        want = [int(x) for x in args.micro_shape.split(",")]
-        shapes = [sh for sh in shapes if list(sh[:4]) == want[:4] and (len(want) < 5 or int(sh[4]) == want[4])]
+        keep = []
+        for spec in args.micro_shape.split(";"):
+            want = [int(x) for x in spec.split(",")]
+            keep += [sh for sh in shapes if list(sh[:4]) == want[:4] and (len(want) < 5 or int(sh[4]) == want[4])]
+        shapes = keep
     for n_win, d, w, k, dyn in shapes:
         rng = np.random.default_rng([args.seed, n_win, d, w, k, int(dyn)])  # per shape: filterable
         sig = d ** -0.25

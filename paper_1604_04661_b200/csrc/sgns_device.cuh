@@ -388,7 +388,7 @@ __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const Mo
                                             int m, int k1, float alpha, bool exact,
                                             const float *sig_s, bool want_loss, double &loss_acc,
                                             long long &cell_acc, const float *rows_s, float *e_s,
-                                            float2 (&hot)[NS]) {
+                                            float2 (&hot)[NS], int kbase = 0) {
   constexpr int NV = 8;
   static_assert(K1R <= NV, "K1R <= 8");
   const int lane = sh.lane;
@@ -425,12 +425,12 @@ __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const Mo
     const int hk = v >> 3, kk = v & 7;
     float er = 0.f, es = 0.f;
     if (kk < k1 && (hk == 0 || two)) {
-      if (exact) cell_error<float>(s, kk, alpha, true, sig_s, er, es);
-      else cell_error_f32(s, kk, alpha, sig_s, er, es);
+      if (exact) cell_error<float>(s, kbase + kk, alpha, true, sig_s, er, es);
+      else cell_error_f32(s, kbase + kk, alpha, sig_s, er, es);
       if ((lane & 1) == 0) {
         e_s[(i + hk) * 8 + kk] = es;
         if (want_loss) {
-          loss_acc += softplus(kk == 0 ? -(double)s : (double)s);
+          loss_acc += softplus(kbase + kk == 0 ? -(double)s : (double)s);
           cell_acc += 1;
         }
       }
@@ -509,6 +509,33 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
   f2_dc<NS, NCH, K1R, EXACT_K>(mv, sh, off_s, m, k1, rows_s, e_s);
 }
 
+
+// float32, 8 < k1 <= 16, d <= 512: window_update_f2 over two groups of output rows
+// (k < 8, then 8 <= k < k1; kbase shifts the label so only k = 0 is positive).  The
+// group's C rows live in registers, so only the m input rows are staged in shared memory
+// (~13 KB per warp at d = 300: 16 warps per SM, where staging all m + k1 rows allows 7);
+// the price is that dA is scattered once per group.  Group 1's rows are loaded before
+// group 0's dC is scattered, so in place (Hogwild) every row is gathered before this
+// window updates it, as batch_core gathers all rows first (kernel_batched.py:104-113).
+template <int NS, int NCH, bool HOT = false>
+__device__ __forceinline__ void window_update_f2g(const ModelView<float> &mv, const uint32_t *off_s,
+                                                  int m, int k1, float alpha, bool exact,
+                                                  const float *sig_s, bool want_loss,
+                                                  double &loss_acc, long long &cell_acc,
+                                                  float *rows_s, float *e_s, int lane,
+                                                  float2 (&hot)[NS]) {
+  const F2Shape<NS, NCH> sh(mv, lane);
+  f2_issue_a<NS, NCH>(mv, sh, off_s, m, rows_s);
+  float2 c[8][NS];
+  f2_load_c<NS, NCH, 8, false>(c, mv, sh, off_s + m, 8);
+  f2_score_da<NS, NCH, 8, false, HOT>(c, mv, sh, off_s, m, 8, alpha, exact, sig_s, want_loss,
+                                      loss_acc, cell_acc, rows_s, e_s, hot, 0);
+  f2_load_c<NS, NCH, 8, false>(c, mv, sh, off_s + m + 8, k1 - 8);
+  f2_dc<NS, NCH, 8, false>(mv, sh, off_s, m, 8, rows_s, e_s);
+  f2_score_da<NS, NCH, 8, false, HOT>(c, mv, sh, off_s, m, k1 - 8, alpha, exact, sig_s, want_loss,
+                                      loss_acc, cell_acc, rows_s, e_s, hot, 8);
+  f2_dc<NS, NCH, 8, false>(mv, sh, off_s + 8, m, k1 - 8, rows_s, e_s);
+}
 
 // float32, 8 < k1 <= 16, d <= 512: like window_update_f2 but the k1 output rows stay in
 // shared memory (16 x NS float2 would not fit in registers).  Each C-row slot load is

@@ -39,13 +39,16 @@ struct Slab {
   int64_t rows, e, ids, roff, kept, off, total;
 };
 // MODE_F2: float32 fast path (only the m input rows are staged); MODE_SMEM: all rows staged
-enum { MODE_SMEM = 0, MODE_F2 = 1, MODE_F2S = 2 };
+// MODE_F2S: float32 8 < k1 <= 16, all rows staged; MODE_F2G: the same k1 in two register groups
+enum { MODE_SMEM = 0, MODE_F2 = 1, MODE_F2S = 2, MODE_F2G = 3 };
 __host__ __device__ inline Slab slab_layout(int mode, int64_t elem, int64_t ld, int mcap, int k1,
                                             int kept_cap) {
   Slab s;
   s.rows = 0;
-  s.e = round16((int64_t)(mode == MODE_F2 ? mcap : mcap + k1) * ld * elem);
-  const int erow = mode == MODE_F2S ? 16 : (k1 > 8 ? k1 : 8);  // F2 error rows padded to 8 / 16
+  const bool a_only = mode == MODE_F2 || mode == MODE_F2G;  // only the input rows are staged
+  s.e = round16((int64_t)(a_only ? mcap : mcap + k1) * ld * elem);
+  // error rows: padded to 8 floats (F2, F2G per group), 16 (F2S), k1 (generic)
+  const int erow = mode == MODE_F2S ? 16 : mode == MODE_F2G ? 8 : (k1 > 8 ? k1 : 8);
   s.ids = s.e + round16((int64_t)2 * mcap * erow * elem);
   s.roff = s.ids + round16((int64_t)(mcap + k1) * 4);
   s.kept = s.roff + round16((int64_t)(mcap + k1) * 4);
@@ -95,6 +98,11 @@ __device__ __forceinline__ void run_window(const ModelView<T> &mv, const int *id
     __syncwarp();
     window_update_f2<NS, NCH, K1R, K1R == 6, HOT>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss,
                                                   cells, rows_s, e_s, lane, hot);
+  } else if constexpr (MODE == MODE_F2G) {
+    for (int r = lane; r < m + k1; r += 32) roff_s[r] = (uint32_t)ids_s[r] * (uint32_t)mv.ld;
+    __syncwarp();
+    window_update_f2g<NS, NCH, HOT>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss, cells,
+                                    rows_s, e_s, lane, hot);
   } else if constexpr (MODE == MODE_F2S) {
     for (int r = lane; r < m + k1; r += 32) roff_s[r] = (uint32_t)ids_s[r] * (uint32_t)mv.ld;
     __syncwarp();
@@ -153,7 +161,7 @@ __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) update_windows
                                            sig_s, want, loss, cells, rows_s, e_s, lane, hot);
   }
 
-  if constexpr (HOT && (MODE == MODE_F2 || MODE == MODE_F2S)) {
+  if constexpr (HOT && (MODE == MODE_F2 || MODE == MODE_F2S || MODE == MODE_F2G)) {
     // the warp's accumulated row-0 dA: one scatter per warp, none when row 0 never occurred
     bool any = false;
 #pragma unroll
@@ -556,6 +564,18 @@ int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident);
 static int ns_for(int64_t ld_elems_f32) { return (int)((ld_elems_f32 / 2 + 31) / 32); }
 static bool offsets32_ok(int64_t vocab, int64_t ld) { return vocab * ld < (int64_t(1) << 32); }
 
+// 8 < k1 <= 16: F2S (all rows staged in shared memory, dA scattered once) while shared
+// memory still allows it as many resident warps as F2G (output rows in two register
+// groups, dA scattered per group); F2G otherwise (configs[1] d = 300, K = 15: 7 vs 16 warps
+// per SM, 0.35 -> 0.50 of the HBM peak).
+template <typename KS, typename KG>
+static bool prefer_staged(KS ks, KG kg, int64_t slab_staged, int64_t slab_groups) {
+  int ws = 0, bs = 0, wg = 0, bg = 0;
+  if (choose_wpb(ks, table_bytes(4), slab_staged, &ws, &bs)) return false;
+  if (choose_wpb(kg, table_bytes(4), slab_groups, &wg, &bg)) return true;
+  return ws * bs >= wg * bg;
+}
+
 #if SGNS_HAS(1)
 template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT = false>
 static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
@@ -608,7 +628,14 @@ static int drive_f2(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
 
 template <int NS, int RNG>
 static int drive_f2s(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
-  return launch_drive_t<float, MODE_F2S, NS, (NS + 1) / 2, 16, RNG>(a, wpb, st, res);
+  constexpr int NCH = (NS + 1) / 2;
+  const int k1 = a.k_neg + 1, mcap = std::min(a.cap, 2 * a.window);
+  if (prefer_staged(drive_kernel<float, MODE_F2S, NS, NCH, 16, RNG>,
+                    drive_kernel<float, MODE_F2G, NS, NCH, 8, RNG>,
+                    slab_layout(MODE_F2S, 4, a.mv.ld, mcap, k1, a.kept_cap).total,
+                    slab_layout(MODE_F2G, 4, a.mv.ld, mcap, k1, a.kept_cap).total))
+    return launch_drive_t<float, MODE_F2S, NS, NCH, 16, RNG>(a, wpb, st, res);
+  return launch_drive_t<float, MODE_F2G, NS, NCH, 8, RNG>(a, wpb, st, res);
 }
 
 template <int RNG>
@@ -677,9 +704,17 @@ static int update_f2(UpdateArgs<float> a, cudaStream_t st) {
 
 template <int NS>
 static int update_f2s(UpdateArgs<float> a, cudaStream_t st) {
+  constexpr int NCH = (NS + 1) / 2;
   const bool hot = static_cast<const float *>(a.mv.in_dst) != a.mv.in_src;  // snapshot mode
-  return hot ? launch_update_t<float, MODE_F2S, NS, (NS + 1) / 2, 16, true>(a, st)
-             : launch_update_t<float, MODE_F2S, NS, (NS + 1) / 2, 16, false>(a, st);
+  const bool staged = prefer_staged(update_windows_kernel<float, MODE_F2S, NS, NCH, 16, false>,
+                                    update_windows_kernel<float, MODE_F2G, NS, NCH, 8, false>,
+                                    slab_layout(MODE_F2S, 4, a.mv.ld, a.mcap, a.k1, 0).total,
+                                    slab_layout(MODE_F2G, 4, a.mv.ld, a.mcap, a.k1, 0).total);
+  if (staged)
+    return hot ? launch_update_t<float, MODE_F2S, NS, NCH, 16, true>(a, st)
+               : launch_update_t<float, MODE_F2S, NS, NCH, 16, false>(a, st);
+  return hot ? launch_update_t<float, MODE_F2G, NS, NCH, 8, true>(a, st)
+             : launch_update_t<float, MODE_F2G, NS, NCH, 8, false>(a, st);
 }
 
 int update_f32(UpdateArgs<float> a, cudaStream_t st) {
