@@ -375,20 +375,31 @@ __device__ __forceinline__ void f2_load_c(float2 (&c)[K1R][NS], const ModelView<
   }
 }
 
-// HOT (snapshot mode only): dA of row 0 -- the most frequent word in the reference's
-// count-sorted vocabulary (corpus.py:86-105), about 8% of all input slots under Zipf --
-// is summed into the warp's register accumulator `hot` instead of being scattered, and
-// the caller adds it to the model once per warp.  Each window's delta is rounded as in
-// the scatter path; only the summation order changes, which the concurrent scatters leave
-// unspecified anyway.  Without it every window's row-0 dA queues on the same few L2
-// lines (per-address serialised red.add).
+// HOT (snapshot mode only): updates of the most frequent rows are summed per warp and
+// added to the model once, at the end of the launch, instead of being scattered window by
+// window.  Under Zipf ids the head rows of the reference's count-sorted vocabulary
+// (corpus.py:86-105) take a large share of all slots -- row 0 about 8% of the inputs --
+// and every scatter to them queues on the same few L2 lines (red.add serialises per
+// address).  Two sinks:
+//  * shared memory (in_s != nullptr): rows [0, H) of both matrices, per warp, in lane-owned
+//    columns, so plain loads/stores suffice; H is what the launch's spare shared memory
+//    holds without costing resident warps;
+//  * registers (in_s == nullptr): row 0 of M_in only (lim = 1), 2 NS registers per lane.
+// Each window's delta is rounded as in the scatter path; only the summation order
+// changes, which the concurrent scatters leave unspecified anyway.
+template <int NS> struct HotSink {
+  float2 reg[NS];
+  float *in_s, *out_s;  // [H][ld] each, this warp's
+  uint32_t lim;         // a row offset (id * ld) below lim is hot
+};
+
 template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT>
 __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const ModelView<float> &mv,
                                             const F2Shape<NS, NCH> &sh, const uint32_t *off_s,
                                             int m, int k1, float alpha, bool exact,
                                             const float *sig_s, bool want_loss, double &loss_acc,
                                             long long &cell_acc, const float *rows_s, float *e_s,
-                                            float2 (&hot)[NS], int kbase = 0) {
+                                            HotSink<NS> &hot, int kbase = 0) {
   constexpr int NV = 8;
   static_assert(K1R <= NV, "K1R <= 8");
   const int lane = sh.lane;
@@ -447,9 +458,19 @@ __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const Mo
         for (int j = 0; j < NS; ++j) d[j] = k == 0 ? __fmul2_rn(ek2, c[0][j]) : __ffma2_rn(ek2, c[k][j], d[j]);
       }
       const uint32_t ro = off_s[i + h];
-      if (HOT && ro == 0) {
+      if (HOT && ro < hot.lim) {
+        if (hot.in_s) {
+          float *hs = hot.in_s + ro + 2 * lane;
 #pragma unroll
-        for (int j = 0; j < NS; ++j) hot[j] = __fadd2_rn(hot[j], __fmul2_rn(d[j], alpha2));
+          for (int j = 0; j < NS; ++j)
+            if (sh.slot_ok(j)) {
+              float2 *q = reinterpret_cast<float2 *>(hs + 64 * j);
+              *q = __fadd2_rn(*q, __fmul2_rn(d[j], alpha2));
+            }
+        } else {
+#pragma unroll
+          for (int j = 0; j < NS; ++j) hot.reg[j] = __fadd2_rn(hot.reg[j], __fmul2_rn(d[j], alpha2));
+        }
       } else {
         float *dst = in_dst_l + ro;
 #pragma unroll
@@ -461,10 +482,10 @@ __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const Mo
   __syncwarp();
 }
 
-template <int NS, int NCH, int K1R, bool EXACT_K>
+template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT = false>
 __device__ __forceinline__ void f2_dc(const ModelView<float> &mv, const F2Shape<NS, NCH> &sh,
                                       const uint32_t *off_s, int m, int k1, const float *rows_s,
-                                      const float *e_s) {
+                                      const float *e_s, HotSink<NS> *hot = nullptr) {
   auto kk_ok = [&](int k) { return EXACT_K || k < k1; };
   float *out_dst_l = mv.out_dst + 2 * sh.lane;
 #pragma unroll
@@ -486,8 +507,16 @@ __device__ __forceinline__ void f2_dc(const ModelView<float> &mv, const F2Shape<
         if (kk_ok(k)) acc[k] = __ffma2_rn(make_float2(ev[k], ev[k]), a0, acc[k]);
     }
 #pragma unroll
-    for (int k = 0; k < K1R; ++k)
-      if (kk_ok(k)) atomicAdd(reinterpret_cast<float2 *>(out_dst_l + off_s[m + k] + 64 * j), acc[k]);
+    for (int k = 0; k < K1R; ++k) {
+      if (!kk_ok(k)) continue;
+      const uint32_t ro = off_s[m + k];
+      if (HOT && hot->out_s && ro < hot->lim) {
+        float2 *q = reinterpret_cast<float2 *>(hot->out_s + ro + col);
+        *q = __fadd2_rn(*q, acc[k]);
+      } else {
+        atomicAdd(reinterpret_cast<float2 *>(out_dst_l + ro + 64 * j), acc[k]);
+      }
+    }
   }
   __syncwarp();
 }
@@ -498,7 +527,7 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
                                                  const float *sig_s, bool want_loss,
                                                  double &loss_acc, long long &cell_acc,
                                                  float *rows_s, float *e_s, int lane,
-                                                 float2 (&hot)[NS]) {
+                                                 HotSink<NS> &hot) {
   if constexpr (EXACT_K) k1 = K1R;
   const F2Shape<NS, NCH> sh(mv, lane);
   f2_issue_a<NS, NCH>(mv, sh, off_s, m, rows_s);
@@ -506,7 +535,7 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
   f2_load_c<NS, NCH, K1R, EXACT_K>(c, mv, sh, off_s + m, k1);
   f2_score_da<NS, NCH, K1R, EXACT_K, HOT>(c, mv, sh, off_s, m, k1, alpha, exact, sig_s, want_loss,
                                           loss_acc, cell_acc, rows_s, e_s, hot);
-  f2_dc<NS, NCH, K1R, EXACT_K>(mv, sh, off_s, m, k1, rows_s, e_s);
+  f2_dc<NS, NCH, K1R, EXACT_K, HOT>(mv, sh, off_s, m, k1, rows_s, e_s, &hot);
 }
 
 
@@ -523,7 +552,7 @@ __device__ __forceinline__ void window_update_f2g(const ModelView<float> &mv, co
                                                   const float *sig_s, bool want_loss,
                                                   double &loss_acc, long long &cell_acc,
                                                   float *rows_s, float *e_s, int lane,
-                                                  float2 (&hot)[NS]) {
+                                                  HotSink<NS> &hot) {
   const F2Shape<NS, NCH> sh(mv, lane);
   f2_issue_a<NS, NCH>(mv, sh, off_s, m, rows_s);
   float2 c[8][NS];
@@ -531,10 +560,10 @@ __device__ __forceinline__ void window_update_f2g(const ModelView<float> &mv, co
   f2_score_da<NS, NCH, 8, false, HOT>(c, mv, sh, off_s, m, 8, alpha, exact, sig_s, want_loss,
                                       loss_acc, cell_acc, rows_s, e_s, hot, 0);
   f2_load_c<NS, NCH, 8, false>(c, mv, sh, off_s + m + 8, k1 - 8);
-  f2_dc<NS, NCH, 8, false>(mv, sh, off_s, m, 8, rows_s, e_s);
+  f2_dc<NS, NCH, 8, false, HOT>(mv, sh, off_s, m, 8, rows_s, e_s, &hot);
   f2_score_da<NS, NCH, 8, false, HOT>(c, mv, sh, off_s, m, k1 - 8, alpha, exact, sig_s, want_loss,
                                       loss_acc, cell_acc, rows_s, e_s, hot, 8);
-  f2_dc<NS, NCH, 8, false>(mv, sh, off_s + 8, m, k1 - 8, rows_s, e_s);
+  f2_dc<NS, NCH, 8, false, HOT>(mv, sh, off_s + 8, m, k1 - 8, rows_s, e_s, &hot);
 }
 
 // float32, 8 < k1 <= 16, d <= 512: like window_update_f2 but the k1 output rows stay in
@@ -548,7 +577,7 @@ __device__ __forceinline__ void window_update_f2s(const ModelView<float> &mv, co
                                                   const float *sig_s, bool want_loss,
                                                   double &loss_acc, long long &cell_acc,
                                                   float *rows_s, float *e_s, int lane,
-                                                  float2 (&hot)[NS]) {
+                                                  HotSink<NS> &hot) {  // register sink only
   constexpr int KM = 16;
   const int64_t ld = mv.ld;
   const int nvec = mv.nvec, nslot = nvec * 2;
@@ -628,8 +657,8 @@ __device__ __forceinline__ void window_update_f2s(const ModelView<float> &mv, co
 #pragma unroll
     for (int j = 0; j < NS; ++j) {
       const float2 u0 = __fmul2_rn(d0[j], alpha2), u1 = __fmul2_rn(d1[j], alpha2);
-      if (hot0) hot[j] = __fadd2_rn(hot[j], u0);
-      if (hot1) hot[j] = __fadd2_rn(hot[j], u1);
+      if (hot0) hot.reg[j] = __fadd2_rn(hot.reg[j], u0);
+      if (hot1) hot.reg[j] = __fadd2_rn(hot.reg[j], u1);
       if (slot_ok(j)) {
         if (!hot0) atomicAdd(reinterpret_cast<float2 *>(dst0 + 64 * j), u0);
         if (two && !hot1) atomicAdd(reinterpret_cast<float2 *>(dst1 + 64 * j), u1);

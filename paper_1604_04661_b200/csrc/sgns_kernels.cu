@@ -36,13 +36,14 @@ __host__ __device__ inline int64_t round16(int64_t b) { return (b + 15) & ~int64
 
 // shared-memory slab of one warp
 struct Slab {
-  int64_t rows, e, ids, roff, kept, off, total;
+  int64_t rows, e, ids, roff, kept, off, hot, total;
 };
 // MODE_F2: float32 fast path (only the m input rows are staged); MODE_SMEM: all rows staged
 // MODE_F2S: float32 8 < k1 <= 16, all rows staged; MODE_F2G: the same k1 in two register groups
 enum { MODE_SMEM = 0, MODE_F2 = 1, MODE_F2S = 2, MODE_F2G = 3 };
+// hot_rows: shared-memory hot-row sink of update_windows (rows [0, H) of both matrices)
 __host__ __device__ inline Slab slab_layout(int mode, int64_t elem, int64_t ld, int mcap, int k1,
-                                            int kept_cap) {
+                                            int kept_cap, int hot_rows = 0) {
   Slab s;
   s.rows = 0;
   const bool a_only = mode == MODE_F2 || mode == MODE_F2G;  // only the input rows are staged
@@ -53,7 +54,8 @@ __host__ __device__ inline Slab slab_layout(int mode, int64_t elem, int64_t ld, 
   s.roff = s.ids + round16((int64_t)(mcap + k1) * 4);
   s.kept = s.roff + round16((int64_t)(mcap + k1) * 4);
   s.off = s.kept + round16((int64_t)kept_cap * 4);
-  s.total = s.off + round16((int64_t)kept_cap * 4);
+  s.hot = s.off + round16((int64_t)kept_cap * 4);
+  s.total = s.hot + round16((int64_t)2 * hot_rows * ld * elem);
   return s;
 }
 __host__ __device__ inline int64_t table_bytes(int64_t elem) { return round16(kSigBins * elem); }
@@ -85,14 +87,14 @@ __device__ __forceinline__ void flush_loss(double loss, long long cells, double 
 
 // K1R == 6 is instantiated for k1 == 6 exactly (K = 5, the north-star shape); K1R == 8
 // covers k1 <= 8 with predicates.
-// HOT: see f2_score_da (float32 k1 <= 16 paths, snapshot mode); `hot` is the warp's row-0
-// dA accumulator, unused otherwise.
+// HOT: see HotSink (sgns_device.cuh; float32 k1 <= 16 paths, snapshot mode); `hot` is
+// the warp's sink, unused otherwise.
 __host__ __device__ constexpr int hot_slots(int ns) { return ns > 0 ? ns : 1; }
 template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT = false>
 __device__ __forceinline__ void run_window(const ModelView<T> &mv, const int *ids_s, uint32_t *roff_s,
                                            int m, int k1, T alpha, bool exact, const T *sig_s,
                                            bool want, double &loss, long long &cells, T *rows_s,
-                                           T *e_s, int lane, float2 (&hot)[hot_slots(NS)]) {
+                                           T *e_s, int lane, HotSink<hot_slots(NS)> &hot) {
   if constexpr (MODE == MODE_F2) {
     for (int r = lane; r < m + k1; r += 32) roff_s[r] = (uint32_t)ids_s[r] * (uint32_t)mv.ld;
     __syncwarp();
@@ -126,6 +128,7 @@ template <typename T> struct UpdateArgs {
   int64_t *loss_cells;
   int32_t *error;
   int wpb;
+  int hot_rows;  // shared-memory hot-row sink rows (HOT launches; 0: register sink, row 0)
 };
 
 template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT>
@@ -134,7 +137,7 @@ __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) update_windows
   T *sig_s = reinterpret_cast<T *>(smem);
   load_table(sig_s, p.sig);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Slab L = slab_layout(MODE, sizeof(T), p.mv.ld, p.mcap, p.k1, 0);
+  const Slab L = slab_layout(MODE, sizeof(T), p.mv.ld, p.mcap, p.k1, 0, HOT ? p.hot_rows : 0);
   unsigned char *base = smem + table_bytes(sizeof(T)) + (int64_t)warp * L.total;
   T *rows_s = reinterpret_cast<T *>(base + L.rows);
   T *e_s = reinterpret_cast<T *>(base + L.e);
@@ -142,9 +145,20 @@ __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) update_windows
   uint32_t *roff_s = reinterpret_cast<uint32_t *>(base + L.roff);
   double loss = 0.0;
   long long cells = 0;
-  float2 hot[hot_slots(NS)];
+  HotSink<hot_slots(NS)> hot;
 #pragma unroll
-  for (int j = 0; j < hot_slots(NS); ++j) hot[j] = make_float2(0.f, 0.f);
+  for (int j = 0; j < hot_slots(NS); ++j) hot.reg[j] = make_float2(0.f, 0.f);
+  hot.in_s = hot.out_s = nullptr;
+  hot.lim = 1;  // register sink: row 0 of M_in
+  if constexpr (HOT) {
+    if (p.hot_rows > 0) {
+      hot.in_s = reinterpret_cast<float *>(base + L.hot);
+      hot.out_s = hot.in_s + (int64_t)p.hot_rows * p.mv.ld;
+      hot.lim = (uint32_t)(p.hot_rows * p.mv.ld);
+      for (int64_t q = lane; q < 2 * (int64_t)p.hot_rows * p.mv.ld; q += 32) hot.in_s[q] = 0.f;
+      __syncwarp();
+    }
+  }
   const int step = gridDim.x * p.wpb;
   for (int w = blockIdx.x * p.wpb + warp; w < p.n_win; w += step) {
     const int lo = p.in_off[w], hi = p.in_off[w + 1];
@@ -162,16 +176,33 @@ __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) update_windows
   }
 
   if constexpr (HOT && (MODE == MODE_F2 || MODE == MODE_F2S || MODE == MODE_F2G)) {
-    // the warp's accumulated row-0 dA: one scatter per warp, none when row 0 never occurred
-    bool any = false;
+    // the warp's sums: one scatter per hot row, none for a row it never updated
+    auto flush = [&](const float2 (&v)[NS], float *row) {
+      bool any = false;
 #pragma unroll
-    for (int j = 0; j < NS; ++j) any |= hot[j].x != 0.f || hot[j].y != 0.f;
-    if (__any_sync(0xffffffffu, any)) {
-      float *dst = reinterpret_cast<float *>(p.mv.in_dst) + 2 * lane;
+      for (int j = 0; j < NS; ++j) any |= v[j].x != 0.f || v[j].y != 0.f;
+      if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
-      for (int j = 0; j < NS; ++j)
-        if (j < NS - 1 || lane + 32 * j < 2 * p.mv.nvec)
-          atomicAdd(reinterpret_cast<float2 *>(dst + 64 * j), hot[j]);
+        for (int j = 0; j < NS; ++j)
+          if (j < NS - 1 || lane + 32 * j < 2 * p.mv.nvec)
+            atomicAdd(reinterpret_cast<float2 *>(row + 2 * lane + 64 * j), v[j]);
+      }
+    };
+    if (hot.in_s) {
+      __syncwarp();
+      for (int r = 0; r < 2 * p.hot_rows; ++r) {
+        const float *src = hot.in_s + (int64_t)r * p.mv.ld + 2 * lane;
+        float2 v[NS];
+#pragma unroll
+        for (int j = 0; j < NS; ++j)
+          v[j] = (j < NS - 1 || lane + 32 * j < 2 * p.mv.nvec)
+                     ? *reinterpret_cast<const float2 *>(src + 64 * j) : make_float2(0.f, 0.f);
+        float *dst = r < p.hot_rows ? reinterpret_cast<float *>(p.mv.in_dst) + (int64_t)r * p.mv.ld
+                                    : reinterpret_cast<float *>(p.mv.out_dst) + (int64_t)(r - p.hot_rows) * p.mv.ld;
+        flush(v, dst);
+      }
+    } else {
+      flush(hot.reg, reinterpret_cast<float *>(p.mv.in_dst));
     }
   }
   if (p.loss_every > 0) flush_loss<T>(loss, cells, p.loss_sum, p.loss_cells, true, lane);
@@ -433,7 +464,7 @@ __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) drive_kernel(D
           if (lane == 0) p.trace_count[wid] = idx + 1;
         }
         if (p.update) {
-          float2 no_hot[hot_slots(NS)];  // in-place training: no deferred rows
+          HotSink<hot_slots(NS)> no_hot;  // in-place training: no deferred rows (HOT = false)
           run_window<T, MODE, NS, NCH, K1R>(p.mv, ids_s, roff_s, mc, k1, alpha_t, p.exact != 0, sig_s,
                                             want, loss, cells, rows_s, e_s, lane, no_hot);
         }
@@ -580,10 +611,26 @@ static bool prefer_staged(KS ks, KG kg, int64_t slab_staged, int64_t slab_groups
 template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT = false>
 static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
   auto kern = update_windows_kernel<T, MODE, NS, NCH, K1R, HOT>;
-  const Slab L = slab_layout(MODE, sizeof(T), a.mv.ld, a.mcap, a.k1, 0);
+  Slab L = slab_layout(MODE, sizeof(T), a.mv.ld, a.mcap, a.k1, 0);
   int wpb = 0, bps = 0;
   int rc = choose_wpb(kern, table_bytes(sizeof(T)), L.total, &wpb, &bps);
   if (rc) return rc;
+  a.hot_rows = 0;
+  if constexpr (HOT && (MODE == MODE_F2 || MODE == MODE_F2G)) {
+    // the largest shared-memory hot-row sink (<= 8 rows per matrix) that keeps every
+    // resident warp; none fits at d = 300 (the register sink covers row 0 there)
+    for (int h : {8, 4, 2, 1}) {
+      const Slab Lh = slab_layout(MODE, sizeof(T), a.mv.ld, a.mcap, a.k1, 0, h);
+      int wh = 0, bh = 0;
+      if (choose_wpb(kern, table_bytes(sizeof(T)), Lh.total, &wh, &bh) == 0 && wh * bh >= wpb * bps) {
+        a.hot_rows = h;
+        L = Lh;
+        wpb = wh;
+        bps = bh;
+        break;
+      }
+    }
+  }
   a.wpb = wpb;
   const int64_t bytes = table_bytes(sizeof(T)) + (int64_t)wpb * L.total;
   if ((rc = prepare(kern, bytes))) return rc;
@@ -998,7 +1045,7 @@ int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, cons
     a.sig = static_cast<const float *>(d_sig_table);
     a.exact = sigmoid_mode == SGNS_SIGMOID_EXACT;
     a.loss_every = loss_every; a.loss_sum = d_loss_sum; a.loss_cells = d_loss_cells;
-    a.error = d_error; a.wpb = 1;
+    a.error = d_error; a.wpb = 1; a.hot_rows = 0;
     if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
     return update_f32(a, st);
   }
@@ -1013,7 +1060,7 @@ int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, cons
     a.sig = static_cast<const double *>(d_sig_table);
     a.exact = sigmoid_mode == SGNS_SIGMOID_EXACT;
     a.loss_every = loss_every; a.loss_sum = d_loss_sum; a.loss_cells = d_loss_cells;
-    a.error = d_error; a.wpb = 1;
+    a.error = d_error; a.wpb = 1; a.hot_rows = 0;
     if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
     return update_f64(a, st);
   }
