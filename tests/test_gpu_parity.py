@@ -175,11 +175,15 @@ def test_disjoint_windows_equal_sequential(dtype, D, k):
 
 
 @pytest.mark.parametrize("dtype,D,k", [("f64", 300, 5), ("f32", 300, 5), ("f32", 100, 12),
-                                       ("f32", 64, 7)])
+                                       ("f32", 64, 7), ("f32", 100, 5), ("f32", 300, 15),
+                                       ("f32", 200, 10)])
 def test_snapshot_conflicting_windows(dtype, D, k):
-    """P3: Zipf-conflicting windows in snapshot mode == snapshot + sum of per-window deltas
-    (float32 snapshot mode sums row 0's dA per warp in registers before one scatter; Zipf(1.3)
-    puts id 0 in ~30% of the slots here)."""
+    """P3: Zipf-conflicting windows in snapshot mode == snapshot + sum of per-window deltas.
+
+    float32 snapshot mode sums the hottest rows per warp before one scatter: rows [0, 8) of
+    both matrices in shared memory where it fits (d = 64, 100, 200), row 0 of M_in in
+    registers otherwise (d = 300); K = 10 / 15 at d >= 200 take the two-register-group body.
+    Zipf(1.3) puts id 0 in ~30% of the slots here."""
     P, O = _pkg(), _oracle()
     from paper_1604_04661_b200.kernel_batched import DeviceWindowBatch, WindowBatch
     from paper_1604_04661_b200.model import DeviceModel, SIGMOID_TABLE_F32, SIGMOID_TABLE_F64
