@@ -9,9 +9,11 @@ fused device driver, then (N > 1) the full model is averaged with NCCL.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 `--impl reference` times the CPU restatement of the reference algorithm
-(oracle/, kind "port": splitmix stream, 10^8-slot negative table, float64
-accumulation, one pthread per host core, Hogwild) on the same corpus, config,
-metric and step definition, on rank 0 only.
+(oracle/, kind "port": splitmix stream, 10^8-slot negative table, the reference's
+default float32 batch_core_blas core, one pthread per host core, Hogwild) on the
+same corpus, config, metric and step definition, on rank 0 only.  On equal cores
+the port runs 1.67x the reference package's own speed
+(profiles/round1_port_calibration.json), so the GPU/CPU ratio is conservative.
 """
 
 from __future__ import annotations
@@ -178,7 +180,8 @@ def shard_of(corpus, world, rank):
 
 # ------------------------------------------------------------------ CPU leg ----
 def cpu_reference_run(corpus, enc, shard, args, seconds=None, steps=None, warmup=0):
-    """The oracle (reference restatement) on host cores: splitmix + slot table, T pthreads."""
+    """The oracle (reference restatement) on host cores: splitmix + slot table, T pthreads, the
+    float32 batch_core_blas core (the reference's default float32 backend, kernel_batched.py:92-144)."""
     from oracle import oracle as O
     from paper_1604_04661_b200.corpus import default_table_length, keep_probabilities
     T = len(os.sched_getaffinity(0))
@@ -201,7 +204,7 @@ def cpu_reference_run(corpus, enc, shard, args, seconds=None, steps=None, warmup
     run = O.OracleRun(ids, sub_off, m_in, m_out, keep_probs=keep, window=WINDOW, negatives=NEG,
                       batch_cap=16, dynamic=True, seed=args.seed, alpha0=ALPHA0, floor_frac=1e-4,
                       total_x_epochs=total, epochs=1, loss_every=100, n_workers=T, slots=slots,
-                      sig_table=SIGMOID_TABLE_F32, refresh_words=10_000)
+                      sig_table=SIGMOID_TABLE_F32, refresh_words=10_000, matmul="blas")
     budget = math.ceil(args.period / T)
     for _ in range(warmup):
         run.advance(budget, T)
@@ -224,7 +227,10 @@ def cpu_reference_run(corpus, enc, shard, args, seconds=None, steps=None, warmup
     read = sum(w.words_read for w in run.workers) - t0_rd
     return {"value": trained / el, "unit": UNIT, "cores": T, "kind": "port",
             "sample": f"{n} steps x {args.period} words read (= {read} read, {trained} trained) of the "
-                      f"same corpus, splitmix + 1e8-slot table, {T} pthreads, float32 model V={V} d={DIM}",
+                      f"same corpus, splitmix + 1e8-slot table, batch_core_blas restatement (the "
+                      f"reference's default float32 core; 1.67x the reference package's own speed on "
+                      f"equal cores, profiles/round1_port_calibration.json), {T} pthreads, float32 "
+                      f"model V={V} d={DIM}",
             "seconds": el, "steps": n}
 
 
@@ -260,8 +266,9 @@ def config_block(args, world):
 
 
 def micro_cpu_leg(base_in, base_out, off, ins, outs, wbytes, wflops, T):
-    """The same windows through the oracle's restatement of the reference core on host
-    threads (test infrastructure as the checker-side baseline; kind "port")."""
+    """The same windows through the oracle's restatement of the reference's default float32
+    core (batch_core_blas) on host threads (test infrastructure as the checker-side
+    baseline; kind "port")."""
     from oracle import oracle as O
     from paper_1604_04661_b200.model import SIGMOID_TABLE_F32
     out = {"kind": "port", "cores_available": T}
@@ -270,7 +277,7 @@ def micro_cpu_leg(base_in, base_out, off, ins, outs, wbytes, wflops, T):
         a, c = base_in.copy(), base_out.copy()
         t0 = time.perf_counter()
         O.process_windows(a, c, off[:n + 1], ins[:off[n]], outs[:n], 0.025, SIGMOID_TABLE_F32,
-                          n_threads=threads)
+                          n_threads=threads, matmul="blas")
         dt = time.perf_counter() - t0
         out[f"threads_{threads}"] = {"sample_windows": n, "windows_per_sec": n / dt,
                                      "alg_GBps": float(wbytes[:n].sum()) / dt / 1e9,

@@ -53,7 +53,7 @@ class Drive(C.Structure):
                 ("loss_every", C.c_int), ("workers", P), ("n_workers", C.c_int),
                 ("word_budget", I64), ("loss_by_epoch", P), ("cells_by_epoch", P),
                 ("update", C.c_int), ("trace_cap", I64), ("trace", P), ("trace_alpha", P),
-                ("trace_count", P), ("position_mode", C.c_int)]
+                ("trace_count", P), ("position_mode", C.c_int), ("matmul", C.c_int)]
 
 
 assert _lib.or_sizeof_worker() == C.sizeof(Worker)
@@ -68,9 +68,10 @@ _lib.or_philox4x32_10.argtypes = [P, P, P]
 _lib.or_sigmoid_table_f32.restype = C.c_float
 _lib.or_sigmoid_table_f32.argtypes = [C.c_float, P]
 _lib.or_process_batch.argtypes = [C.c_int, P, P, I64, C.c_int, P, C.c_int, P, C.c_int, F64,
-                                  C.c_int, P]
+                                  C.c_int, P, C.c_int]
 _lib.or_process_windows.argtypes = [C.c_int, P, P, I64, C.c_int, P, P, P, I64, C.c_int, F64,
-                                    C.c_int, P, C.c_int]
+                                    C.c_int, P, C.c_int, C.c_int]
+MATMUL = {"naive": 0, "blas": 1}
 _lib.or_init_model.argtypes = [I64, C.c_int, U64, P]
 _lib.or_neg_boundaries.argtypes = [P, I64, F64, I64, P]
 _lib.or_drive.argtypes = [C.POINTER(Drive), C.c_int]
@@ -111,21 +112,22 @@ def sigmoid_table_f32(x: float, table: np.ndarray) -> np.float32:
 
 
 def process_batch(m_in: np.ndarray, m_out: np.ndarray, in_ids, out_ids, alpha: float,
-                  table: np.ndarray) -> None:
-    """batch_core_naive in place; float64 models use the exact sigmoid (as the reference)."""
+                  table: np.ndarray, matmul: str = "naive") -> None:
+    """batch_core_naive in place (matmul="blas": the float32 batch_core_blas restatement);
+    float64 models use the exact sigmoid (as the reference)."""
     assert m_in.flags.c_contiguous and m_out.flags.c_contiguous and m_in.dtype == m_out.dtype
     dtype = 1 if m_in.dtype == np.float64 else 0
     ins = np.ascontiguousarray(in_ids, dtype=np.int32)
     outs = np.ascontiguousarray(out_ids, dtype=np.int32)
     tab = np.ascontiguousarray(table, dtype=m_in.dtype)
     _lib.or_process_batch(dtype, _p(m_in), _p(m_out), m_in.shape[1], m_in.shape[1], _p(ins),
-                          len(ins), _p(outs), len(outs), float(alpha), dtype, _p(tab))
+                          len(ins), _p(outs), len(outs), float(alpha), dtype, _p(tab), MATMUL[matmul])
 
 
 def process_windows(m_in: np.ndarray, m_out: np.ndarray, in_off, in_ids, out_ids, alpha: float,
-                    table: np.ndarray, n_threads: int = 1) -> None:
+                    table: np.ndarray, n_threads: int = 1, matmul: str = "naive") -> None:
     """Packed windows in place (out_ids n_win x K1); n_threads Hogwild threads on contiguous
-    window ranges; one thread == sequential process_batch calls."""
+    window ranges; one thread == sequential process_batch calls.  matmul as process_batch."""
     assert m_in.flags.c_contiguous and m_out.flags.c_contiguous and m_in.dtype == m_out.dtype
     dtype = 1 if m_in.dtype == np.float64 else 0
     off = np.ascontiguousarray(in_off, dtype=np.int32)
@@ -137,7 +139,7 @@ def process_windows(m_in: np.ndarray, m_out: np.ndarray, in_off, in_ids, out_ids
     assert outs.size == n_win * k1
     if _lib.or_process_windows(dtype, _p(m_in), _p(m_out), m_in.shape[1], m_in.shape[1], _p(off),
                                _p(ins), _p(outs), n_win, k1, float(alpha), dtype, _p(tab),
-                               int(n_threads)) != 0:
+                               int(n_threads), MATMUL[matmul]) != 0:
         raise MemoryError("or_process_windows")
 
 
@@ -178,7 +180,7 @@ class OracleRun:
                  dynamic, seed, alpha0, floor_frac, total_x_epochs, epochs, loss_every,
                  n_workers, sent_range=None, stream_base=0, rng_mode="splitmix", slots=None,
                  alias=None, sig_table=None, refresh_words=10_000, trace_cap=0, update=True,
-                 use_exact=None, position_mode=False):
+                 use_exact=None, position_mode=False, matmul="naive"):
         self.ids = np.ascontiguousarray(ids, dtype=np.int32)
         self.offsets = np.ascontiguousarray(offsets, dtype=np.int64)
         self.m_in, self.m_out = m_in, m_out
@@ -234,6 +236,7 @@ class OracleRun:
         d.trace_alpha = _p(self.trace_alpha)
         d.trace_count = _p(self.trace_count)
         d.position_mode = int(position_mode)
+        d.matmul = MATMUL[matmul] if d.dtype == 0 else 0
         self.d = d
 
     @property

@@ -62,7 +62,7 @@ def main():
                               negatives=5, batch_cap=16, dynamic=True, seed=seed, alpha0=0.025,
                               floor_frac=1e-4, total_x_epochs=float(syn.encoded.n_tokens) * args.epochs,
                               epochs=args.epochs, loss_every=1, n_workers=T, slots=slots,
-                              sig_table=SIGMOID_TABLE_F32)
+                              sig_table=SIGMOID_TABLE_F32, matmul="blas")
             t1 = time.perf_counter()
             orc.run_to_completion(n_threads=T)
             wall = time.perf_counter() - t1
