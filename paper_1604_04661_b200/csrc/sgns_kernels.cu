@@ -608,6 +608,13 @@ static bool prefer_staged(KS ks, KG kg, int64_t slab_staged, int64_t slab_groups
 }
 
 #if SGNS_HAS(1)
+// Both matrices gathered from a separate source (snapshot mode): the hot-row sinks may
+// defer the hottest rows' updates to the end of the launch (see HotSink).
+static bool snapshot_mode(const ModelView<float> &mv) {
+  return static_cast<const float *>(mv.in_dst) != mv.in_src &&
+         static_cast<const float *>(mv.out_dst) != mv.out_src;
+}
+
 template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT = false>
 static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
   auto kern = update_windows_kernel<T, MODE, NS, NCH, K1R, HOT>;
@@ -740,8 +747,7 @@ static int drive_f64(DriveArgs<double> a, int wpb, cudaStream_t st, int *res) {
 template <int NS>
 static int update_f2(UpdateArgs<float> a, cudaStream_t st) {
   constexpr int NCH = (NS + 1) / 2;
-  // snapshot mode (rows gathered from a separate source): row 0's dA is combined per warp
-  const bool hot = static_cast<const float *>(a.mv.in_dst) != a.mv.in_src;
+  const bool hot = snapshot_mode(a.mv);
   if (a.k1 == 6)
     return hot ? launch_update_t<float, MODE_F2, NS, NCH, 6, true>(a, st)
                : launch_update_t<float, MODE_F2, NS, NCH, 6, false>(a, st);
@@ -752,7 +758,7 @@ static int update_f2(UpdateArgs<float> a, cudaStream_t st) {
 template <int NS>
 static int update_f2s(UpdateArgs<float> a, cudaStream_t st) {
   constexpr int NCH = (NS + 1) / 2;
-  const bool hot = static_cast<const float *>(a.mv.in_dst) != a.mv.in_src;  // snapshot mode
+  const bool hot = snapshot_mode(a.mv);
   const bool staged = prefer_staged(update_windows_kernel<float, MODE_F2S, NS, NCH, 16, false>,
                                     update_windows_kernel<float, MODE_F2G, NS, NCH, 8, false>,
                                     slab_layout(MODE_F2S, 4, a.mv.ld, a.mcap, a.k1, 0).total,
