@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--seeds", type=int, default=1)
     ap.add_argument("--epochs", type=int, default=5)
     ap.add_argument("--tokens", type=int, default=17_000_000)
+    ap.add_argument("--vocab", type=int, default=71_000,
+                    help="raw ids (configs[2]: 71k; configs[3]: 1M with --tokens 800M --epochs 1)")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
     import paper_1604_04661_b200 as P
@@ -35,14 +37,15 @@ def main():
     from paper_1604_04661_b200.synthetic import make_planted_corpus
 
     t0 = time.perf_counter()
-    syn = make_planted_corpus(args.tokens, 71_000, zipf_s=1.05, min_count=5, seed=0)
+    syn = make_planted_corpus(args.tokens, args.vocab, zipf_s=1.05, min_count=5, seed=0)
     gen = time.perf_counter() - t0
     pairs = syn.gold_pairs(pairs_per_cluster=16)
     counts = syn.vocab.counts
     V, D = len(counts), 300
     T = len(os.sched_getaffinity(0))
-    report = {"config": "configs[2] mid: 17M tokens Zipf(1.05) over 71k ids, planted clusters, min-count 5, "
-                        f"d=300 w=5 K=5 t=1e-4, {args.epochs} epochs", "vocab": V,
+    report = {"config": f"{args.tokens:,} tokens Zipf(1.05) over {args.vocab:,} raw ids, planted clusters, "
+                        f"min-count 5, d=300 w=5 K=5 t=1e-4, {args.epochs} epochs "
+                        "(configs[2]: 17M / 71k / 5 epochs; configs[3]: 800M / 1M / 1 epoch)", "vocab": V,
               "tokens": syn.encoded.n_tokens, "corpus_gen_s": gen, "host_cores": T, "runs": []}
     for seed in range(1, args.seeds + 1):
         cfg = P.TrainingConfig(dim=D, window=5, negatives=5, subsample=1e-4, min_count=5, alpha0=0.025,
