@@ -28,6 +28,9 @@ def main():
     ap.add_argument("--vocab", type=int, default=71_000,
                     help="raw ids (configs[2]: 71k; configs[3]: 1M with --tokens 800M --epochs 1)")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--gpu-rng", choices=["philox", "splitmix"], default="philox",
+                    help="splitmix: the reference's stream + 1e8-slot table on the GPU (static schedule)")
+    ap.add_argument("--gpu-workers", type=int, default=0, help="0: the config default")
     args = ap.parse_args()
     import paper_1604_04661_b200 as P
     from oracle import oracle as O
@@ -49,10 +52,11 @@ def main():
               "tokens": syn.encoded.n_tokens, "corpus_gen_s": gen, "host_cores": T, "runs": []}
     for seed in range(1, args.seeds + 1):
         cfg = P.TrainingConfig(dim=D, window=5, negatives=5, subsample=1e-4, min_count=5, alpha0=0.025,
-                               epochs=args.epochs, seed=seed, loss_sample_every=1)
+                               epochs=args.epochs, seed=seed, loss_sample_every=1, rng=args.gpu_rng,
+                               workers=args.gpu_workers or None)
         model, st = P.train_encoded(syn.vocab, syn.encoded, cfg)
         rho_g = similarity_score(model.input_vectors, syn.vocab.index, pairs)[0] / 100
-        run = {"seed": seed, "gpu": {"words_per_sec": st.throughput_words_per_sec, "wall_s": st.wall_seconds,
+        run = {"seed": seed, "gpu_rng": args.gpu_rng, "gpu": {"words_per_sec": st.throughput_words_per_sec, "wall_s": st.wall_seconds,
                                      "loss_by_epoch": st.loss_by_epoch, "rho": rho_g,
                                      "words_trained": st.words_processed}}
         if not args.skip_cpu:
