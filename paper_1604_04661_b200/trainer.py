@@ -66,7 +66,7 @@ class TrainingConfig:
     dynamic_window: bool = True
     table_length: int | None = None
     float64: bool = False
-    matmul: str | None = None  # None / "cuda"
+    matmul: str | None = None  # None / "cuda" / the reference's "blas" | "naive" (all the CUDA core)
     loss_sample_every: int = 100
     # device knobs (new)
     rng: str = "philox"                   # "philox" (production) | "splitmix" (reference stream)
@@ -99,7 +99,7 @@ class TrainingConfig:
             raise ConfigError("batch_cap must be >= 1")
         if self.kernel != "batched":
             raise ConfigError(f"unknown kernel {self.kernel!r} (the device path is 'batched')")
-        if self.matmul not in (None, "cuda"):
+        if self.matmul not in (None, "cuda", "blas", "naive"):
             raise ConfigError(f"unknown matmul backend {self.matmul!r}")
         if self.rng not in ("philox", "splitmix"):
             raise ConfigError(f"unknown rng {self.rng!r}")

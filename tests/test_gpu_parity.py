@@ -95,7 +95,9 @@ def test_process_batch_validation():
     with pytest.raises(ValueError):
         P.process_batch(m, P.Minibatch([1], [0, 2]), -0.1)
     with pytest.raises(ValueError):
-        P.process_batch(m, P.Minibatch([1], [0, 2]), 0.1, matmul="blas")
+        P.process_batch(m, P.Minibatch([1], [0, 2]), 0.1, matmul="magic")
+    P.process_batch(m, P.Minibatch([1], [0, 2]), 0.1, matmul="blas")  # reference names accepted
+    P.process_batch(m, P.Minibatch([1], [0, 2]), 0.1, matmul="naive")
     with pytest.raises(ValueError):
         P.Minibatch([1], [3, 3])
     with pytest.raises(ValueError):
