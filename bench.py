@@ -262,7 +262,9 @@ def config_block(args, world):
             "parallelism": f"dp{world}",
             "sync": "full model every period" if args.sync_hot_rows < 0 else
                     f"rows [0,{args.sync_hot_rows}) + round-robin chunk every period",
-            "l2": "model 2.4 GB and corpus 3.2 GB exceed the 126 MB L2; no flush between steps"}
+            "l2": "model 2.4 GB and corpus 3.2 GB exceed the 126 MB L2; no flush between steps",
+            **({"dist_backend": os.environ["SGNS_BENCH_DIST_BACKEND"] + " (plumbing check, not a measurement)"}
+               if os.environ.get("SGNS_BENCH_DIST_BACKEND", "nccl") != "nccl" else {})}
 
 
 def micro_cpu_leg(base_in, base_out, off, ins, outs, wbytes, wflops, T):
@@ -382,11 +384,20 @@ def main():
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    # SGNS_BENCH_DIST_BACKEND=gloo: plumbing check of the N > 1 path with several ranks sharing
+    # fewer GPUs (host-staged averaging; the ranks' kernels never wait on each other).  Not a
+    # measurement: the line says so in config.dist_backend.
+    backend = os.environ.get("SGNS_BENCH_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     from paper_1604_04661_b200 import _lib
     from paper_1604_04661_b200.distributed import NcclTransport, scaled_alpha0
     from paper_1604_04661_b200.model import init_device_model
