@@ -381,16 +381,17 @@ __device__ __forceinline__ void f2_load_c(float2 (&c)[K1R][NS], const ModelView<
 // (corpus.py:86-105) take a large share of all slots -- row 0 about 8% of the inputs --
 // and every scatter to them queues on the same few L2 lines (red.add serialises per
 // address).  Two sinks:
-//  * shared memory (in_s != nullptr): rows [0, H) of both matrices, per warp, in lane-owned
-//    columns, so plain loads/stores suffice; H is what the launch's spare shared memory
-//    holds without costing resident warps;
-//  * registers (in_s == nullptr): row 0 of M_in only (lim = 1), 2 NS registers per lane.
+//  * shared memory: rows [0, H_in) of M_in (in_s) and [0, H_out) of M_out (out_s), per warp,
+//    in lane-owned columns, so plain loads/stores suffice; H_in / H_out are what the
+//    launch's spare shared memory holds without costing resident warps;
+//  * registers (in_s == nullptr): row 0 of M_in (in_lim = 1), 2 NS registers per lane, when
+//    no M_in row fits in shared memory (M_out row 0 may still have a shared-memory sink).
 // Each window's delta is rounded as in the scatter path; only the summation order
 // changes, which the concurrent scatters leave unspecified anyway.
 template <int NS> struct HotSink {
   float2 reg[NS];
-  float *in_s, *out_s;  // [H][ld] each, this warp's
-  uint32_t lim;         // a row offset (id * ld) below lim is hot
+  float *in_s, *out_s;       // [H_in][ld], [H_out][ld]: this warp's (nullptr: none)
+  uint32_t in_lim, out_lim;  // a row offset (id * ld) below the limit is hot
 };
 
 template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT>
@@ -458,7 +459,7 @@ __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const Mo
         for (int j = 0; j < NS; ++j) d[j] = k == 0 ? __fmul2_rn(ek2, c[0][j]) : __ffma2_rn(ek2, c[k][j], d[j]);
       }
       const uint32_t ro = off_s[i + h];
-      if (HOT && ro < hot.lim) {
+      if (HOT && ro < hot.in_lim) {
         if (hot.in_s) {
           float *hs = hot.in_s + ro + 2 * lane;
 #pragma unroll
@@ -510,7 +511,7 @@ __device__ __forceinline__ void f2_dc(const ModelView<float> &mv, const F2Shape<
     for (int k = 0; k < K1R; ++k) {
       if (!kk_ok(k)) continue;
       const uint32_t ro = off_s[m + k];
-      if (HOT && hot->out_s && ro < hot->lim) {
+      if (HOT && ro < hot->out_lim) {
         float2 *q = reinterpret_cast<float2 *>(hot->out_s + ro + col);
         *q = __fadd2_rn(*q, acc[k]);
       } else {

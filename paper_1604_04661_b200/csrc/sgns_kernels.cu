@@ -41,7 +41,7 @@ struct Slab {
 // MODE_F2: float32 fast path (only the m input rows are staged); MODE_SMEM: all rows staged
 // MODE_F2S: float32 8 < k1 <= 16, all rows staged; MODE_F2G: the same k1 in two register groups
 enum { MODE_SMEM = 0, MODE_F2 = 1, MODE_F2S = 2, MODE_F2G = 3 };
-// hot_rows: shared-memory hot-row sink of update_windows (rows [0, H) of both matrices)
+// hot_rows: shared-memory hot-row sink rows of update_windows (H_in + H_out rows, see HotSink)
 __host__ __device__ inline Slab slab_layout(int mode, int64_t elem, int64_t ld, int mcap, int k1,
                                             int kept_cap, int hot_rows = 0) {
   Slab s;
@@ -50,12 +50,13 @@ __host__ __device__ inline Slab slab_layout(int mode, int64_t elem, int64_t ld, 
   s.e = round16((int64_t)(a_only ? mcap : mcap + k1) * ld * elem);
   // error rows: padded to 8 floats (F2, F2G per group), 16 (F2S), k1 (generic)
   const int erow = mode == MODE_F2S ? 16 : mode == MODE_F2G ? 8 : (k1 > 8 ? k1 : 8);
-  s.ids = s.e + round16((int64_t)2 * mcap * erow * elem);
+  // F2 / F2G keep only the scaled errors; the other bodies keep raw and scaled
+  s.ids = s.e + round16((int64_t)(a_only ? 1 : 2) * mcap * erow * elem);
   s.roff = s.ids + round16((int64_t)(mcap + k1) * 4);
   s.kept = s.roff + round16((int64_t)(mcap + k1) * 4);
   s.off = s.kept + round16((int64_t)kept_cap * 4);
   s.hot = s.off + round16((int64_t)kept_cap * 4);
-  s.total = s.hot + round16((int64_t)2 * hot_rows * ld * elem);
+  s.total = s.hot + round16((int64_t)hot_rows * ld * elem);
   return s;
 }
 __host__ __device__ inline int64_t table_bytes(int64_t elem) { return round16(kSigBins * elem); }
@@ -128,7 +129,7 @@ template <typename T> struct UpdateArgs {
   int64_t *loss_cells;
   int32_t *error;
   int wpb;
-  int hot_rows;  // shared-memory hot-row sink rows (HOT launches; 0: register sink, row 0)
+  int hot_in, hot_out;  // shared-memory hot-row sink rows (HOT launches; hot_in 0: register sink)
 };
 
 template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT>
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) update_windows
   T *sig_s = reinterpret_cast<T *>(smem);
   load_table(sig_s, p.sig);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Slab L = slab_layout(MODE, sizeof(T), p.mv.ld, p.mcap, p.k1, 0, HOT ? p.hot_rows : 0);
+  const Slab L = slab_layout(MODE, sizeof(T), p.mv.ld, p.mcap, p.k1, 0, HOT ? p.hot_in + p.hot_out : 0);
   unsigned char *base = smem + table_bytes(sizeof(T)) + (int64_t)warp * L.total;
   T *rows_s = reinterpret_cast<T *>(base + L.rows);
   T *e_s = reinterpret_cast<T *>(base + L.e);
@@ -149,15 +150,20 @@ __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) update_windows
 #pragma unroll
   for (int j = 0; j < hot_slots(NS); ++j) hot.reg[j] = make_float2(0.f, 0.f);
   hot.in_s = hot.out_s = nullptr;
-  hot.lim = 1;  // register sink: row 0 of M_in
+  hot.in_lim = 1;  // register sink: row 0 of M_in
+  hot.out_lim = 0;
   if constexpr (HOT) {
-    if (p.hot_rows > 0) {
-      hot.in_s = reinterpret_cast<float *>(base + L.hot);
-      hot.out_s = hot.in_s + (int64_t)p.hot_rows * p.mv.ld;
-      hot.lim = (uint32_t)(p.hot_rows * p.mv.ld);
-      for (int64_t q = lane; q < 2 * (int64_t)p.hot_rows * p.mv.ld; q += 32) hot.in_s[q] = 0.f;
-      __syncwarp();
+    float *hs = reinterpret_cast<float *>(base + L.hot);
+    if (p.hot_in > 0) {
+      hot.in_s = hs;
+      hot.in_lim = (uint32_t)(p.hot_in * p.mv.ld);
     }
+    if (p.hot_out > 0) {
+      hot.out_s = hs + (int64_t)p.hot_in * p.mv.ld;
+      hot.out_lim = (uint32_t)(p.hot_out * p.mv.ld);
+    }
+    for (int64_t q = lane; q < (int64_t)(p.hot_in + p.hot_out) * p.mv.ld; q += 32) hs[q] = 0.f;
+    __syncwarp();
   }
   const int step = gridDim.x * p.wpb;
   for (int w = blockIdx.x * p.wpb + warp; w < p.n_win; w += step) {
@@ -188,21 +194,19 @@ __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) update_windows
             atomicAdd(reinterpret_cast<float2 *>(row + 2 * lane + 64 * j), v[j]);
       }
     };
-    if (hot.in_s) {
-      __syncwarp();
-      for (int r = 0; r < 2 * p.hot_rows; ++r) {
-        const float *src = hot.in_s + (int64_t)r * p.mv.ld + 2 * lane;
-        float2 v[NS];
+    __syncwarp();
+    if (!hot.in_s) flush(hot.reg, reinterpret_cast<float *>(p.mv.in_dst));
+    const float *hs = reinterpret_cast<const float *>(base + L.hot);
+    for (int r = 0; r < p.hot_in + p.hot_out; ++r) {
+      const float *src = hs + (int64_t)r * p.mv.ld + 2 * lane;
+      float2 v[NS];
 #pragma unroll
-        for (int j = 0; j < NS; ++j)
-          v[j] = (j < NS - 1 || lane + 32 * j < 2 * p.mv.nvec)
-                     ? *reinterpret_cast<const float2 *>(src + 64 * j) : make_float2(0.f, 0.f);
-        float *dst = r < p.hot_rows ? reinterpret_cast<float *>(p.mv.in_dst) + (int64_t)r * p.mv.ld
-                                    : reinterpret_cast<float *>(p.mv.out_dst) + (int64_t)(r - p.hot_rows) * p.mv.ld;
-        flush(v, dst);
-      }
-    } else {
-      flush(hot.reg, reinterpret_cast<float *>(p.mv.in_dst));
+      for (int j = 0; j < NS; ++j)
+        v[j] = (j < NS - 1 || lane + 32 * j < 2 * p.mv.nvec)
+                   ? *reinterpret_cast<const float2 *>(src + 64 * j) : make_float2(0.f, 0.f);
+      float *dst = r < p.hot_in ? reinterpret_cast<float *>(p.mv.in_dst) + (int64_t)r * p.mv.ld
+                                : reinterpret_cast<float *>(p.mv.out_dst) + (int64_t)(r - p.hot_in) * p.mv.ld;
+      flush(v, dst);
     }
   }
   if (p.loss_every > 0) flush_loss<T>(loss, cells, p.loss_sum, p.loss_cells, true, lane);
@@ -622,15 +626,17 @@ static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
   int wpb = 0, bps = 0;
   int rc = choose_wpb(kern, table_bytes(sizeof(T)), L.total, &wpb, &bps);
   if (rc) return rc;
-  a.hot_rows = 0;
+  a.hot_in = a.hot_out = 0;
   if constexpr (HOT && (MODE == MODE_F2 || MODE == MODE_F2G)) {
-    // the largest shared-memory hot-row sink (<= 8 rows per matrix) that keeps every
-    // resident warp; none fits at d = 300 (the register sink covers row 0 there)
-    for (int h : {8, 4, 2, 1}) {
-      const Slab Lh = slab_layout(MODE, sizeof(T), a.mv.ld, a.mcap, a.k1, 0, h);
+    // the largest shared-memory hot-row sink that keeps every resident warp: rows [0, H) of
+    // both matrices (H <= 8), else M_out's row 0 beside the register sink for M_in's row 0
+    const int cand[5][2] = {{8, 8}, {4, 4}, {2, 2}, {1, 1}, {0, 1}};
+    for (const auto &hc : cand) {
+      const Slab Lh = slab_layout(MODE, sizeof(T), a.mv.ld, a.mcap, a.k1, 0, hc[0] + hc[1]);
       int wh = 0, bh = 0;
       if (choose_wpb(kern, table_bytes(sizeof(T)), Lh.total, &wh, &bh) == 0 && wh * bh >= wpb * bps) {
-        a.hot_rows = h;
+        a.hot_in = hc[0];
+        a.hot_out = hc[1];
         L = Lh;
         wpb = wh;
         bps = bh;
@@ -1051,7 +1057,7 @@ int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, cons
     a.sig = static_cast<const float *>(d_sig_table);
     a.exact = sigmoid_mode == SGNS_SIGMOID_EXACT;
     a.loss_every = loss_every; a.loss_sum = d_loss_sum; a.loss_cells = d_loss_cells;
-    a.error = d_error; a.wpb = 1; a.hot_rows = 0;
+    a.error = d_error; a.wpb = 1; a.hot_in = a.hot_out = 0;
     if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
     return update_f32(a, st);
   }
@@ -1066,7 +1072,7 @@ int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, cons
     a.sig = static_cast<const double *>(d_sig_table);
     a.exact = sigmoid_mode == SGNS_SIGMOID_EXACT;
     a.loss_every = loss_every; a.loss_sum = d_loss_sum; a.loss_cells = d_loss_cells;
-    a.error = d_error; a.wpb = 1; a.hot_rows = 0;
+    a.error = d_error; a.wpb = 1; a.hot_in = a.hot_out = 0;
     if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
     return update_f64(a, st);
   }
