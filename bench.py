@@ -53,6 +53,8 @@ def parse():
                     help="--config micro: id distribution (uniform = no hot rows, diagnostic)")
     ap.add_argument("--micro-shape", default="",
                     help="--config micro: run only shapes matching 'n_win,d,w,K[,dyn]' (e.g. 65536,300,5,5), ';'-separated, in that order")
+    ap.add_argument("--micro-no-flush", action="store_true",
+                    help="--config micro diagnostic: no L2 flush between launches (not the configs[1] protocol)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--sync-hot-rows", type=int, default=-1,
@@ -350,7 +352,8 @@ def micro_bench(args):
               for _ in range(args.steps)]
         flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
         for i in range(args.steps):
-            flush.add_(1.0)  # 256 MB write between launches: L2 flushed
+            if not args.micro_no_flush:
+                flush.add_(1.0)  # 256 MB write between launches: L2 flushed
             ev[i][0].record(st)
             update_windows(dst, dwb, 0.025, src=src)
             ev[i][1].record(st)
@@ -364,7 +367,8 @@ def micro_bench(args):
                 "inputs_per_window": float(ms.mean()), "us_per_launch": t * 1e6,
                 "windows_per_sec": n_win / t, "alg_GBps": by / t / 1e9,
                 "frac_of_peak": by / t / 1e9 / peak, "peak": peak, "peak_source": peak_kind,
-                "GFLOPs": fl / t / 1e9, "l2": "flushed (256 MB write) before every launch"}
+                "GFLOPs": fl / t / 1e9,
+                "l2": "NOT flushed (diagnostic)" if args.micro_no_flush else "flushed (256 MB write) before every launch"}
         if not args.no_cpu_baseline:
             line["cpu_reference"] = micro_cpu_leg(base_in, base_out, off, ins, outs, wbytes, wflops, T)
         print(json.dumps(line), flush=True)
