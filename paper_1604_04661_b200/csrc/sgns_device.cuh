@@ -547,24 +547,26 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
 // the price is that dA is scattered once per group.  Group 1's rows are loaded before
 // group 0's dC is scattered, so in place (Hogwild) every row is gathered before this
 // window updates it, as batch_core gathers all rows first (kernel_batched.py:104-113).
-template <int NS, int NCH, bool HOT = false>
+template <int NS, int NCH, int K1R2 = 8, bool HOT = false>
 __device__ __forceinline__ void window_update_f2g(const ModelView<float> &mv, const uint32_t *off_s,
                                                   int m, int k1, float alpha, bool exact,
                                                   const float *sig_s, bool want_loss,
                                                   double &loss_acc, long long &cell_acc,
                                                   float *rows_s, float *e_s, int lane,
                                                   HotSink<NS> &hot) {
+  // K1R2: register rows of the second group (4 when k1 <= 12, else 8)
   const F2Shape<NS, NCH> sh(mv, lane);
   f2_issue_a<NS, NCH>(mv, sh, off_s, m, rows_s);
   float2 c[8][NS];
   f2_load_c<NS, NCH, 8, false>(c, mv, sh, off_s + m, 8);
   f2_score_da<NS, NCH, 8, false, HOT>(c, mv, sh, off_s, m, 8, alpha, exact, sig_s, want_loss,
                                       loss_acc, cell_acc, rows_s, e_s, hot, 0);
-  f2_load_c<NS, NCH, 8, false>(c, mv, sh, off_s + m + 8, k1 - 8);
+  float2 c2[K1R2][NS];
+  f2_load_c<NS, NCH, K1R2, false>(c2, mv, sh, off_s + m + 8, k1 - 8);
   f2_dc<NS, NCH, 8, false, HOT>(mv, sh, off_s, m, 8, rows_s, e_s, &hot);
-  f2_score_da<NS, NCH, 8, false, HOT>(c, mv, sh, off_s, m, k1 - 8, alpha, exact, sig_s, want_loss,
-                                      loss_acc, cell_acc, rows_s, e_s, hot, 8);
-  f2_dc<NS, NCH, 8, false, HOT>(mv, sh, off_s + 8, m, k1 - 8, rows_s, e_s, &hot);
+  f2_score_da<NS, NCH, K1R2, false, HOT>(c2, mv, sh, off_s, m, k1 - 8, alpha, exact, sig_s, want_loss,
+                                         loss_acc, cell_acc, rows_s, e_s, hot, 8);
+  f2_dc<NS, NCH, K1R2, false, HOT>(mv, sh, off_s + 8, m, k1 - 8, rows_s, e_s, &hot);
 }
 
 // float32, 8 < k1 <= 16, d <= 512: like window_update_f2 but the k1 output rows stay in

@@ -104,8 +104,8 @@ __device__ __forceinline__ void run_window(const ModelView<T> &mv, const int *id
   } else if constexpr (MODE == MODE_F2G) {
     for (int r = lane; r < m + k1; r += 32) roff_s[r] = (uint32_t)ids_s[r] * (uint32_t)mv.ld;
     __syncwarp();
-    window_update_f2g<NS, NCH, HOT>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss, cells,
-                                    rows_s, e_s, lane, hot);
+    window_update_f2g<NS, NCH, K1R, HOT>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss, cells,
+                                         rows_s, e_s, lane, hot);
   } else if constexpr (MODE == MODE_F2S) {
     for (int r = lane; r < m + k1; r += 32) roff_s[r] = (uint32_t)ids_s[r] * (uint32_t)mv.ld;
     __syncwarp();
@@ -695,6 +695,8 @@ static int drive_f2s(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
                     slab_layout(MODE_F2S, 4, a.mv.ld, mcap, k1, a.kept_cap).total,
                     slab_layout(MODE_F2G, 4, a.mv.ld, mcap, k1, a.kept_cap).total))
     return launch_drive_t<float, MODE_F2S, NS, NCH, 16, RNG>(a, wpb, st, res);
+  // F2G's K1R: rows of its second output group
+  if (k1 <= 12) return launch_drive_t<float, MODE_F2G, NS, NCH, 4, RNG>(a, wpb, st, res);
   return launch_drive_t<float, MODE_F2G, NS, NCH, 8, RNG>(a, wpb, st, res);
 }
 
@@ -772,6 +774,10 @@ static int update_f2s(UpdateArgs<float> a, cudaStream_t st) {
   if (staged)
     return hot ? launch_update_t<float, MODE_F2S, NS, NCH, 16, true>(a, st)
                : launch_update_t<float, MODE_F2S, NS, NCH, 16, false>(a, st);
+  // F2G's K1R: rows of its second output group
+  if (a.k1 <= 12)
+    return hot ? launch_update_t<float, MODE_F2G, NS, NCH, 4, true>(a, st)
+               : launch_update_t<float, MODE_F2G, NS, NCH, 4, false>(a, st);
   return hot ? launch_update_t<float, MODE_F2G, NS, NCH, 8, true>(a, st)
              : launch_update_t<float, MODE_F2G, NS, NCH, 8, false>(a, st);
 }
