@@ -166,10 +166,10 @@ __device__ __forceinline__ void select_negatives(const FastArgs &p, NegCand cnd,
 #endif
 // FULL: the row holds exactly 32 * NS float2 slots (ld padded, e.g. 320 at d = 300), so
 // every lane owns NS whole slots and no per-slot predicate is needed.
-// Register cap: 128 (16 warps per SM) while the K1R x NS float2 output rows fit.  The padded
-// K1R = 8 variant (k1 = 7, 8) at NS >= 5 (d > 256) spills under 128 (72-byte stack at
-// d = 300, 144-424 bytes above), so it takes up to 168 registers (12-13 warps per SM):
-// K = 6 / 7 on the configs[2] corpus 142 / 139 -> 158 / 156 M words/s.
+// Register cap: 128 (16 warps per SM) while the K1R x NS float2 output rows fit.  K1R = 7, 8
+// (k1 = 7, 8) at NS >= 5 (d > 256) would spill under 128 (72-byte stack at d = 300 for the
+// earlier padded K1R = 8 build, 144-424 bytes above), so they take up to 168 registers
+// (12-13 warps per SM): K = 6 / 7 on the configs[2] corpus 142 / 139 -> 158 / 156 M words/s.
 template <int NS, int K1R> struct FastRegs {
   static constexpr int v = (K1R > 6 && NS >= 5) ? SGNS_FAST_MAXNREG_WIDE : SGNS_FAST_MAXNREG;
 };

@@ -919,11 +919,21 @@ static int launch_fast_t(FastArgs a, int wpb_req, cudaStream_t st, int *resident
 template <int NS>
 static int fast_ns(FastArgs a, int wpb, cudaStream_t st, int *res) {
   const bool full = a.mv.ld == 64 * NS;  // 32 lanes x NS float2 slots exactly
-  if (a.k_neg + 1 == 6)
-    return full ? launch_fast_t<NS, 6, true, true>(a, wpb, st, res)
-                : launch_fast_t<NS, 6, true, false>(a, wpb, st, res);
-  return full ? launch_fast_t<NS, 8, false, true>(a, wpb, st, res)
-              : launch_fast_t<NS, 8, false, false>(a, wpb, st, res);
+  // exact-K instantiations for K + 1 = 4..8 (no per-output predicates); K + 1 < 4 pads to 6
+  switch (a.k_neg + 1) {
+    case 4: return full ? launch_fast_t<NS, 4, true, true>(a, wpb, st, res)
+                        : launch_fast_t<NS, 4, true, false>(a, wpb, st, res);
+    case 5: return full ? launch_fast_t<NS, 5, true, true>(a, wpb, st, res)
+                        : launch_fast_t<NS, 5, true, false>(a, wpb, st, res);
+    case 6: return full ? launch_fast_t<NS, 6, true, true>(a, wpb, st, res)
+                        : launch_fast_t<NS, 6, true, false>(a, wpb, st, res);
+    case 7: return full ? launch_fast_t<NS, 7, true, true>(a, wpb, st, res)
+                        : launch_fast_t<NS, 7, true, false>(a, wpb, st, res);
+    case 8: return full ? launch_fast_t<NS, 8, true, true>(a, wpb, st, res)
+                        : launch_fast_t<NS, 8, true, false>(a, wpb, st, res);
+  }
+  return full ? launch_fast_t<NS, 6, false, true>(a, wpb, st, res)
+              : launch_fast_t<NS, 6, false, false>(a, wpb, st, res);
 }
 
 int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
