@@ -379,12 +379,14 @@ def test_fast_driver_windows_match_oracle(workers):
     assert run.words_trained == orc.workers[0].words_trained
 
 
-@pytest.mark.parametrize("D,k", [(64, 5), (300, 7), (512, 2), (100, 3), (320, 5), (4, 6)])
+@pytest.mark.parametrize("D,k", [(64, 5), (300, 7), (512, 2), (100, 3), (320, 5), (4, 6),
+                                 (200, 4), (300, 6)])
 def test_fast_driver_single_worker_trains_like_oracle(D, k):
     """One worker, dynamic schedule: same windows in the same order -> fp32 model within
     accumulated rounding of the oracle's float64-accumulating restatement; loss within 1e-3.
-    Covers the fast kernel's variants: exact K1 = 6 and padded K1R = 8, whole-slot rows
-    (d = 64, 320, 512) and partial last slots (d = 4, 100, 300)."""
+    Covers the fast kernel's variants: exact K1 = 4..8 (k = 3..7), K1 < 4 padded to 6
+    (k = 2), whole-slot rows (d = 64, 320, 512) and partial last slots (d = 4, 100, 200,
+    300)."""
     P = _pkg()
     from paper_1604_04661_b200.synthetic import make_planted_corpus
     from paper_1604_04661_b200.model import DeviceModel
