@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SGNS_ABI_VERSION 1
+#define SGNS_ABI_VERSION 2
 
 enum {
   SGNS_OK = 0,
@@ -126,6 +126,10 @@ typedef struct sgns_drive_params {
    * double[1] = {loss_sum}; the caller zeroes them before the launch. */
   int64_t *d_totals;
   double *d_loss_total;
+  /* optional: touched-row map, uint8[2 * vocab] = {M_in rows, M_out rows}; every window
+   * sets the bytes of its m input rows and k + 1 output rows to 1 (plain stores, never
+   * cleared by the kernels).  Data-parallel touched-row averaging reads it. */
+  uint8_t *d_dirty;
 } sgns_drive_params;
 
 enum { SGNS_SCHEDULE_STATIC = 0, SGNS_SCHEDULE_DYNAMIC = 1 };
@@ -172,10 +176,12 @@ void sgns_encoded_free(sgns_encoded *e);
 /* ---- word2vec vector files (sgns_io.cpp) ----
  * save_model (model.py:118-139) byte for byte: "V D\n" then per word the token, a space,
  * and either D "%.6g" values (text) or D little-endian float32 (binary), then "\n".
- * rows: (V, ld) float32, in device memory when rows_on_device != 0 (streamed D2H). */
+ * rows: (V, ld) of dtype SGNS_F32 / SGNS_F64, in device memory when rows_on_device != 0
+ * (streamed D2H).  Text formats the row's own value (a float64 model's double, as the
+ * reference formats model.input_vectors[i]); binary always writes float32 ("<f4"). */
 int sgns_write_vectors(const char *path, const char *tokens_blob, const int64_t *token_offsets,
-                       int64_t vocab, int32_t dim, const float *rows, int64_t ld, int32_t binary,
-                       int32_t rows_on_device);
+                       int64_t vocab, int32_t dim, const void *rows, int64_t ld, int32_t binary,
+                       int32_t rows_on_device, int32_t dtype);
 
 const char *sgns_error_string(int32_t code);
 int sgns_abi_version(void);

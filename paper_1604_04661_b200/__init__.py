@@ -9,7 +9,7 @@ libsgns_b200.so in this directory); there is no CPU fallback.
 from .corpus import (EncodedCorpus, NegativeTable, Vocabulary, build_negative_table, build_vocab,
                      build_vocab_file, encode_corpus, encode_corpus_file, keep_probability,
                      partition_sentences, read_tokens, split_by_tokens)
-from .distributed import (DistributedRunError, NcclTransport, SyncPolicy, Transport,
+from .distributed import (DistributedRunError, HostStagedTransport, NcclTransport, SyncPolicy, Transport,
                           TransportError, distributed_train, partition_corpus, scaled_alpha0,
                           select_sync_rows)
 from .kernel_batched import Minibatch, WindowBatch, process_batch, update_windows
@@ -22,7 +22,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "ConfigError", "DeviceModel", "DeviceRun", "DistributedRunError", "EmbeddingModel",
-    "EncodedCorpus", "Minibatch", "NcclTransport", "NegativeTable", "SyncPolicy",
+    "EncodedCorpus", "HostStagedTransport", "Minibatch", "NcclTransport", "NegativeTable", "SyncPolicy",
     "TrainingConfig", "TrainingStats", "Transport", "TransportError", "Vocabulary",
     "WindowBatch", "build_negative_table", "build_vocab", "distributed_train", "encode_corpus",
     "init_device_model", "init_model", "keep_probability", "partition_corpus", "save_model",

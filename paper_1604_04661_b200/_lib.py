@@ -44,6 +44,7 @@ class DriveParams(C.Structure):
         ("warps_per_block", I32), ("token_base", I64), ("epoch_base", I32),
         ("schedule", I32), ("d_claim", P), ("claim_end", I64), ("shard_lo", I64),
         ("shard_hi", I64), ("words_base", I64), ("d_totals", P), ("d_loss_total", P),
+        ("d_dirty", P),
     ]
 
 
@@ -95,10 +96,10 @@ def lib() -> C.CDLL:
     L.sgns_encoded_free.restype = None
     L.sgns_encoded_free.argtypes = [P]
     L.sgns_write_vectors.restype = C.c_int
-    L.sgns_write_vectors.argtypes = [C.c_char_p, P, P, I64, I32, P, I64, I32, I32]
+    L.sgns_write_vectors.argtypes = [C.c_char_p, P, P, I64, I32, P, I64, I32, I32, I32]
     L.sgns_struct_sizes.restype = C.c_int
     L.sgns_struct_sizes.argtypes = [C.POINTER(I32), C.POINTER(I32)]
-    if L.sgns_abi_version() != 1:
+    if L.sgns_abi_version() != 2:
         raise LibraryMissing("libsgns_b200.so ABI version mismatch; rebuild")
     wb, pb = I32(0), I32(0)
     L.sgns_struct_sizes(C.byref(wb), C.byref(pb))

@@ -27,6 +27,9 @@ constexpr uint64_t kMix2 = 0x94D049BB133111EBULL;
 constexpr uint32_t kTagSub = 0x53554230u;  // 'SUB0'
 constexpr uint32_t kTagWin = 0x57494E30u;  // 'WIN0'
 constexpr uint32_t kTagNeg = 0x4E000000u;
+// negative draws: counter word 2 = kTagNeg | chunk (8 bits) << 16 | attempt pair (16 bits),
+// so a unit may consume at most 2^17 candidate draws (device error 3 past that)
+constexpr uint32_t kMaxNegAttempts = 1u << 17;
 constexpr int kSigBins = 1000;
 
 template <typename T> struct Vec;

@@ -55,6 +55,7 @@ struct FastArgs {
   int64_t words_base;
   unsigned long long *totals;  // optional, see sgns_drive_params.d_totals
   double *loss_total;
+  uint8_t *dirty;              // optional touched-row map [2 * vocab]
 };
 
 struct FastSlab {
@@ -153,6 +154,15 @@ __device__ __forceinline__ void select_negatives(const FastArgs &p, NegCand cnd,
     need -= take;
     if (need == 0) break;
     attempt += (uint32_t)span;  // every candidate of this span was consumed
+    if (attempt >= kMaxNegAttempts) {
+      // the counter holds 17 attempt bits: past them the candidate stream would repeat
+      // (a target carrying almost all of the count^0.75 mass).  Flag it; fill the rest
+      // deterministically so the launch still terminates.
+      if (lane == 0 && p.error) atomicExch(p.error, 3);
+      for (int r = lane; r < need; r += 32)
+        ids_s[mc + 1 + (p.k_neg - need) + r] = (target + 1 + r) % (int)p.vocab;
+      break;
+    }
     span = min(32, need + 2);
     cnd = lane < span ? neg_candidate(p, tok, ep, ch, attempt + lane) : no_candidate();
   }
@@ -339,6 +349,9 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
 #pragma unroll
         for (int j = 0; j < NCH; ++j)
           if (chunk_ok(j)) cp_async16(dst + 128 * j, src + 128 * j);
+      }
+      if (p.dirty != nullptr) {  // touched rows (data-parallel touched-row averaging)
+        for (int r = lane; r < m + k1; r += 32) p.dirty[(r < m ? 0u : p.vocab) + (uint32_t)ids_s[r]] = 1;
       }
       // next unit + its negative candidates (alias loads in flight during u's math)
       Unit nx;

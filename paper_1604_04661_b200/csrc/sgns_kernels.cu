@@ -245,6 +245,7 @@ template <typename T> struct DriveArgs {
   int wpb;
   int64_t token_base;
   uint32_t epoch_base;
+  uint8_t *dirty;  // optional touched-row map [2 * vocab]
 };
 
 // Splitmix stream window: 32 consecutive draws evaluated by the 32 lanes.
@@ -443,10 +444,20 @@ __global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) drive_kernel(D
           if (RNG == SGNS_RNG_SPLITMIX) sb.used = consumed_to;
           else attempt += (uint32_t)consumed_to;
           need -= take;
+          if (RNG != SGNS_RNG_SPLITMIX && need > 0 && attempt >= kMaxNegAttempts) {
+            // 17 attempt bits in the Philox counter: flag instead of cycling forever
+            if (lane == 0 && p.error) atomicExch(p.error, 3);
+            for (int r = lane; r < need; r += 32)
+              ids_s[mc + 1 + (p.k_neg - need) + r] = (target + 1 + r) % (int)p.vocab;
+            need = 0;
+          }
         }
         __syncwarp();
         kc += 1;
         inputs += mc;
+        if (p.dirty != nullptr) {  // touched rows (data-parallel touched-row averaging)
+          for (int r = lane; r < mc + k1; r += 32) p.dirty[(r < mc ? 0u : p.vocab) + (uint32_t)ids_s[r]] = 1;
+        }
         const bool want = p.loss_every > 0 && (kc % p.loss_every) == 0;
         if (p.trace_cap > 0) {
           int64_t idx = p.trace_count[wid];
@@ -874,6 +885,7 @@ static void fill_drive_args(DriveArgs<T> &a, const sgns_drive_params *p) {
   a.error = p->d_error;
   a.token_base = p->token_base;
   a.epoch_base = (uint32_t)p->epoch_base;
+  a.dirty = p->d_dirty;
 }
 
 int drive_static(const sgns_drive_params *p, cudaStream_t st, int *resident) {
@@ -978,6 +990,7 @@ int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
   a.words_base = p->words_base;
   a.totals = reinterpret_cast<unsigned long long *>(p->d_totals);
   a.loss_total = p->d_loss_total;
+  a.dirty = p->d_dirty;
   const int wpb = p->warps_per_block;
   switch (ns_for(p->ld)) {
     case 1: return fast_ns<1>(a, wpb, st, resident);

@@ -120,10 +120,13 @@ def current_stream_ptr(device=None) -> int:
 class DeviceModel:
     """M_in / M_out resident in HBM as (V, ld) tensors."""
 
-    def __init__(self, m_in, m_out, dim: int):
+    def __init__(self, m_in, m_out, dim: int, storage=None):
         self.m_in = m_in
         self.m_out = m_out
         self.dim = dim
+        # (2, V, ld) tensor holding both matrices back to back when allocated here: a
+        # full-model average is then a single collective on one contiguous buffer
+        self.storage = storage
 
     @property
     def vocab_size(self) -> int:
@@ -147,8 +150,8 @@ class DeviceModel:
         torch = _torch()
         ld = padded_ld(dim, dtype)
         td = _tdtype(torch, dtype)
-        return cls(torch.zeros((vocab_size, ld), dtype=td, device=device),
-                   torch.zeros((vocab_size, ld), dtype=td, device=device), dim)
+        st = torch.zeros((2, vocab_size, ld), dtype=td, device=device)
+        return cls(st[0], st[1], dim, st)
 
     @classmethod
     def from_host(cls, model: EmbeddingModel, device="cuda") -> "DeviceModel":
@@ -167,6 +170,9 @@ class DeviceModel:
         model.output_vectors[...] = self.m_out[:, :self.dim].cpu().numpy()
 
     def clone(self) -> "DeviceModel":
+        if self.storage is not None:
+            st = self.storage.clone()
+            return DeviceModel(st[0], st[1], self.dim, st)
         return DeviceModel(self.m_in.clone(), self.m_out.clone(), self.dim)
 
 
@@ -211,16 +217,18 @@ def save_model(model, vocab, path: str, binary: bool = False) -> None:
     offs = np.zeros(len(enc) + 1, dtype=np.int64)
     offs[1:] = np.cumsum([len(t) for t in enc])
     blob = C.create_string_buffer(b"".join(enc), max(int(offs[-1]), 1))
-    if isinstance(model, DeviceModel) and model.np_dtype == np.float32:
+    if isinstance(model, DeviceModel):
         rows, ld, on_dev, keep = model.m_in.data_ptr(), model.ld, 1, model.m_in
+        dt = model.cdtype
         import torch
         torch.cuda.synchronize(model.m_in.device)
     else:
-        host = model.to_host() if isinstance(model, DeviceModel) else model
-        arr = np.ascontiguousarray(host.input_vectors, dtype=np.float32)
+        f64 = model.input_vectors.dtype == np.float64
+        arr = np.ascontiguousarray(model.input_vectors, dtype=np.float64 if f64 else np.float32)
         rows, ld, on_dev, keep = arr.ctypes.data, arr.shape[1], 0, arr
+        dt = _lib.SGNS_F64 if f64 else _lib.SGNS_F32
     rc = _lib.lib().sgns_write_vectors(path.encode(), C.addressof(blob), offs.ctypes.data, vocab.size,
-                                       model.dim, rows, ld, int(binary), on_dev)
+                                       model.dim, rows, ld, int(binary), on_dev, dt)
     del keep
     if rc == -5:
         raise OSError(f"cannot write {path}")

@@ -45,6 +45,14 @@ WORKER_DTYPE = np.dtype([
     ("kernel_counter", "<i8"), ("words_read", "<i8"), ("words_trained", "<i8"), ("inputs", "<i8")])
 
 
+DEVICE_ERRORS = {
+    1: "a window with no inputs or more inputs than the staging holds",
+    2: "sentence longer than the kept-token buffer",
+    3: "negative sampling drew 2^17 candidates without finding K words different from the "
+       "target (the target holds almost all of the count^0.75 mass)",
+}
+
+
 class ConfigError(ValueError):
     """Invalid training configuration."""
 
@@ -109,6 +117,10 @@ class TrainingConfig:
             raise ConfigError("alpha_refresh_words must be >= 1")
         if self.schedule not in ("auto", "static", "dynamic"):
             raise ConfigError(f"unknown schedule {self.schedule!r}")
+        if self.rng == "philox" and -(-2 * self.window // self.batch_cap) > 256:
+            # the Philox negative counter keeps 8 bits of the chunk index (csrc/sgns_device.cuh)
+            raise ConfigError("rng='philox' supports at most 256 chunks per position "
+                              "(ceil(2 * window / batch_cap) <= 256)")
         if self.schedule == "dynamic" and not self.dynamic_eligible(0):
             raise ConfigError("schedule='dynamic' needs rng='philox', float32, negatives <= 7, dim <= 512")
 
@@ -246,7 +258,8 @@ class DeviceRun:
     def __init__(self, model: DeviceModel, corpus: DeviceCorpus, sampler: DeviceSampler,
                  keep_probs: np.ndarray | None, config: TrainingConfig, alpha0_eff: float,
                  total_x_epochs: float, n_workers: int, sent_range: tuple[int, int] | None = None,
-                 stream_base: int = 0, trace_cap: int = 0, update: bool = True):
+                 stream_base: int = 0, trace_cap: int = 0, update: bool = True,
+                 track_dirty: bool = False):
         torch = _torch()
         self.torch = torch
         corpus.check_vocab(model.vocab_size)
@@ -312,6 +325,11 @@ class DeviceRun:
             p.d_trace, p.d_trace_alpha = self.trace.data_ptr(), self.trace_alpha.data_ptr()
             p.d_trace_count = self.trace_count.data_ptr()
         p.d_error = self.error.data_ptr()
+        # touched-row map (M_in rows, M_out rows) for data-parallel touched-row averaging
+        self.dirty = None
+        if track_dirty:
+            self.dirty = torch.zeros((2, model.vocab_size), dtype=torch.uint8, device=dev)
+            p.d_dirty = self.dirty.data_ptr()
         self.dynamic = config.use_dynamic(model.vocab_size)
         if self.dynamic:
             # sentence ordinals c in [0, epochs * n) of the shard, claimed by the workers
@@ -371,7 +389,11 @@ class DeviceRun:
                 return
             total = min(int(word_budget) * self.n_workers, 2**62)
             end = self._claim_end(total)
-            self.claim.fill_(self.claim_pos)
+            if stream is None:
+                self.claim.fill_(self.claim_pos)
+            else:  # the claim counter is reset on the launch's own stream
+                with self.torch.cuda.stream(self.torch.cuda.ExternalStream(st, device=self.device)):
+                    self.claim.fill_(self.claim_pos)
             self.params.claim_end = end
             self._dyn_read += self.words_at(end) - self.words_at(self.claim_pos)
             self.claim_pos = end
@@ -383,7 +405,7 @@ class DeviceRun:
             self._host_state = self.workers.cpu().numpy().view(WORKER_DTYPE).copy()
             err = int(self.error.item())
             if err:
-                raise RuntimeError(f"sgns_drive device error {err} (sentence too long / bad window)")
+                raise RuntimeError(f"sgns_drive device error {err}: {DEVICE_ERRORS.get(err, 'unknown')}")
         return self._host_state
 
     @property

@@ -384,12 +384,27 @@ def gen_io():
         rm.save_model(model, voc, path, binary=binary)
         with open(path, "rb") as fh:
             out[f"bytes_{int(binary)}"] = np.frombuffer(fh.read(), dtype=np.uint8)
+    # float64 model: the reference formats the float64 value itself (%.6g); values sit next
+    # to a 6th-digit rounding boundary, where a float32 cast would print differently
+    v64 = rng.normal(size=(V, D)) * 10.0 ** rng.integers(-5, 5, size=(V, D))
+    v64[1, :] = [1.2345650000000001, 1.2345649999999999, 0.30000000000000004, 2.5e-300,
+                 9.9999995e-5, 123456.49999999999, -7.77777750000001]
+    out["vecs64"] = v64
+    model64 = rm.EmbeddingModel(v64, np.zeros_like(v64))
+    for binary in (False, True):
+        path = os.path.join("/tmp", f"golden_vec64_{int(binary)}")
+        rm.save_model(model64, voc, path, binary=binary)
+        with open(path, "rb") as fh:
+            out[f"bytes64_{int(binary)}"] = np.frombuffer(fh.read(), dtype=np.uint8)
     np.savez_compressed(os.path.join(HERE, "io.npz"), **out)
 
 
 if __name__ == "__main__":
     assert sgns.__version__
+    only = set(sys.argv[1:])  # e.g. "gen_io": regenerate one fixture
     for fn in (gen_rng, gen_tables, gen_init, gen_kernel, gen_traces, gen_train, gen_dist, gen_eval,
                gen_ingest, gen_io, gen_eval_full):
+        if only and fn.__name__ not in only:
+            continue
         fn()
         print("wrote", fn.__name__)

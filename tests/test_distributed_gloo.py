@@ -105,11 +105,22 @@ class OracleEngine:
         self.model.m_out = torch.from_numpy(self.m_out_np)
         self.model.to_host = lambda: (self.m_in_np.copy(), self.m_out_np.copy())
 
+        # touched-row map for SyncPolicy(touched_rows=True): the oracle marks rows whose
+        # value changed in a launch (a touched row left unchanged averages to itself too)
+        self.dirty = torch.zeros((2, V), dtype=torch.uint8)
+
+    def _mark(self, fn):
+        before = (self.m_in_np.copy(), self.m_out_np.copy())
+        fn()
+        for w, (old, new) in enumerate(zip(before, (self.m_in_np, self.m_out_np))):
+            changed = torch.from_numpy((old != new).any(axis=1).astype(np.uint8))
+            self.dirty[w] |= changed
+
     def launch(self, budget):
-        self.run.advance(budget)
+        self._mark(lambda: self.run.advance(budget))
 
     def run_to_completion(self):
-        self.run.run_to_completion()
+        self._mark(self.run.run_to_completion)
 
     @property
     def words_trained(self):
@@ -159,3 +170,49 @@ def test_distributed_train_two_ranks_matches_reference(tmp_path):
     assert r[0]["stats"].tolist() == st[:2].tolist()
     assert r[1]["stats"].tolist() == st[2:].tolist()
     np.testing.assert_allclose(r[0]["loss"], d["dp2_loss0"], rtol=1e-12)
+
+
+def _touched_worker(rank, world, port, out, touched, hot, rot, f64):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import paper_1604_04661_b200 as P
+    from paper_1604_04661_b200.corpus import EncodedCorpus, Vocabulary
+    _init(rank, world, port)
+    g = load_golden("train")
+    enc = EncodedCorpus(g["ids"], g["offsets"], g["sentence_bytes"])
+    vocab = Vocabulary.from_counts(g["counts"])
+    cfg = P.TrainingConfig(dim=8, window=3, negatives=3, subsample=1e-3, min_count=1, epochs=2,
+                           threads=1, seed=4, float64=f64, rng="splitmix")
+    pol = P.SyncPolicy(period_words=1500, hot_rows=hot, rotation_chunk=rot, touched_rows=touched)
+    tr = P.NcclTransport()
+    calls = []
+    orig = tr.average_packed
+    tr.average_packed = lambda parts: (calls.append(sum(int(i.numel()) for _, i in parts)), orig(parts))
+    (m_in, m_out), stats = P.distributed_train(None, cfg, pol, tr, prebuilt=(vocab, enc),
+                                               run_factory=OracleEngine)
+    np.savez(f"{out}_{rank}.npz", m_in=m_in, m_out=m_out, packed=np.array(calls, dtype=np.int64))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("hot,rot,f64", [(None, 0, False), (20, 30, False), (20, 30, True)],
+                         ids=["full_f32", "submodel_f32", "submodel_f64"])
+def test_touched_row_sync_equals_full_sync(tmp_path, hot, rot, f64):
+    """SyncPolicy(touched_rows=True): only rows some rank wrote since their last average go
+    on the wire (flag union = all_reduce MAX, one packed collective); at N = 2 the models
+    are bit-identical to averaging every selected row."""
+    from paper_1604_04661_b200.corpus import Vocabulary
+    V = Vocabulary.from_counts(load_golden("train")["counts"]).size
+    hot = V if hot is None else hot
+    res = {}
+    for touched in (False, True):
+        port = _free_port()
+        out = str(tmp_path / f"t{int(touched)}")
+        mp.spawn(_touched_worker, args=(2, port, out, touched, hot, rot, f64), nprocs=2, join=True)
+        res[touched] = [np.load(f"{out}_{k}.npz") for k in range(2)]
+    for k in range(2):
+        assert np.array_equal(res[True][k]["m_in"], res[False][k]["m_in"])
+        assert np.array_equal(res[True][k]["m_out"], res[False][k]["m_out"])
+    packed = res[True][0]["packed"]
+    assert len(packed) > 2
+    assert packed.max() <= 2 * V and packed[:-1].mean() < 2 * min(V, hot + rot)  # fewer rows moved

@@ -1,0 +1,125 @@
+"""Pins the timed production kernel (drive_fast_kernel, csrc/sgns_fast.cuh) at the
+north-star tolerance, window stream by window stream, and the device sigma-bin rule at
+the reference's 3,008 edge probes.
+
+Per-sentence protocol (test_fast_kernel_per_sentence_vs_oracle).  One worker on the
+dynamic schedule trains exactly one sentence per `DeviceRun.advance(1)`; the kernel
+traces every window it applies (target, inputs, target + negatives, alpha).  Starting
+from the GPU model before the sentence, the pinned oracle (`process_batch`, the
+restatement of batch_core_naive, sgns/kernel_batched.py:147-211, bit-exact against the
+reference's own outputs in tests/test_oracle_golden.py) replays those windows in order,
+and the GPU model after the sentence must equal it at
+
+    |gpu - oracle| <= 1e-5 |oracle| + 1e-7          (tests/test_acceptance.py:199-209)
+
+on every entry.  The vocabulary is tiny (12 ids), so consecutive windows of a sentence
+share their target and negative rows all the time: the kernel's u -> u+1 output-row
+prefetch and its collision patch (sgns_fast.cuh:494-504) are exercised on most windows
+(the test counts them).  batch_cap = 4 splits positions into chunks that share the
+target.  A sentence whose replay meets a score within the float32 rounding distance
+of a sigma-bin edge (oracle/pin.py near_edge) may
+legally differ (SURVEY 8c bin-flip protocol): it is counted and skipped, and both sides
+restart from the GPU state at the next sentence.  The per-sentence loss proxy (float64
+softplus on pre-update scores, sgns/kernel_scalar.py:38-51) is compared at rtol 1e-5.
+"""
+
+import numpy as np
+import pytest
+
+from helpers import load_golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    torch.cuda.set_device(0)
+
+
+def _fast_run(ids, off, counts, dm, *, k, cap, window=5, seed=9, alpha0=0.025):
+    import paper_1604_04661_b200 as P
+    from paper_1604_04661_b200.corpus import EncodedCorpus
+    from paper_1604_04661_b200.trainer import DeviceCorpus, DeviceRun, DeviceSampler
+    enc = EncodedCorpus(ids, off, np.zeros(len(off) - 1, np.int64))
+    cfg = P.TrainingConfig(dim=dm.dim, window=window, negatives=k, batch_cap=cap, dynamic_window=True,
+                           subsample=0.0, seed=seed, epochs=1, rng="philox", workers=1, min_count=1,
+                           loss_sample_every=1, alpha0=alpha0, schedule="dynamic")
+    corpus = DeviceCorpus(enc)
+    sampler = DeviceSampler(counts, "philox")
+    trace_cap = len(ids) * (-(-2 * window // cap)) + 16
+    run = DeviceRun(dm, corpus, sampler, None, cfg, alpha0, float(off[-1]), 1, trace_cap=trace_cap)
+    assert run.dynamic, "the dynamic (fast) driver must be the one under test"
+    return run
+
+
+# (D, K, batch_cap): exact K + 1 = 4..8 instantiations, K + 1 < 4 padded to 6; whole-slot rows
+# (d = 64, 320, 512) and partial last slots (d = 4, 100, 300); cap 4 splits positions.
+CASES = [(d, k, 16) for d in (100, 300, 512) for k in (3, 4, 5, 6, 7)]
+CASES += [(4, 5, 16), (4, 7, 16), (64, 2, 16), (320, 5, 16), (300, 5, 4), (100, 7, 4), (512, 3, 4)]
+
+
+@pytest.mark.parametrize("D,k,cap", CASES, ids=[f"d{d}_k{k}_cap{c}" for d, k, c in CASES])
+def test_fast_kernel_per_sentence_vs_oracle(D, k, cap):
+    import paper_1604_04661_b200 as P
+    from paper_1604_04661_b200.model import DeviceModel, SIGMOID_TABLE_F32
+    from oracle import pin
+    rng = np.random.default_rng(1000 * D + 10 * k + cap)
+    V, n_sent = 12, 60
+    ids, off, counts = pin.tiny_corpus(rng, V, n_sent, 4, 12)
+    scale = 0.6 * D ** -0.25  # scores ~ N(0, 0.36): most cells inside the table's [-6, 6)
+    m_in = (rng.normal(size=(V, D)) * scale).astype(np.float32)
+    m_out = (rng.normal(size=(V, D)) * scale).astype(np.float32)
+    dm = DeviceModel.from_host(P.EmbeddingModel(m_in, m_out))
+    run = _fast_run(ids, off, counts, dm, k=k, cap=cap)
+    t = pin.replay_sentences(run, dm, n_sent, cap, k + 1, SIGMOID_TABLE_F32)
+    assert run.done
+    assert t["windows"] > 200 and t["shared_next"] > t["windows"] // 2, t
+    assert t["compared"] >= 0.7 * n_sent, t  # the rest hold a score at a sigma-bin edge
+    assert t["loss_worst"] <= 1.0, t
+    assert t["worst"] <= 1.0, t
+
+
+@pytest.mark.parametrize("D", [4, 300])
+def test_device_sigma_bins_at_edge_probes(D):
+    """sgns/model.py:108-115 computes the bin index (x + 6) * (1000 / 12) in float64; the
+    device computes it in FP32 and falls back to FP64 within 1e-3 of an integer
+    (cell_error_f32, csrc/sgns_device.cuh, shared by every float32 window body and by
+    drive_fast_kernel).  Each probe x is made an exact score: input row a = [x, 1, x, 0..],
+    target row [1, 0, 0, 0..] (score x), negative row [0, 0, 1, 0..] (score x).  With
+    alpha = 1 the second column of the target / negative output rows receives exactly
+    alpha * err = fl(1 - sigma(x)) / -sigma(x), so both cells' errors are read back bit for
+    bit and compared with the reference's sigmoid_from_table on the same probes."""
+    import paper_1604_04661_b200 as P
+    from paper_1604_04661_b200.kernel_batched import DeviceWindowBatch, WindowBatch
+    from paper_1604_04661_b200.model import DeviceModel
+    g = load_golden("tables")
+    xs = g["probe_x"].astype(np.float32)
+    sig = g["probe_sig"].astype(np.float32)
+    n = len(xs)
+    assert n == 3008
+    V = 3 * n
+    m_in = np.zeros((V, D), np.float32)
+    m_out = np.zeros((V, D), np.float32)
+    ins = np.arange(n, dtype=np.int32)
+    tgt = n + ins
+    neg = 2 * n + ins
+    m_in[ins, 0] = xs
+    m_in[ins, 1] = 1.0
+    m_in[ins, 2] = xs
+    m_out[tgt, 0] = 1.0
+    m_out[neg, 2] = 1.0
+    wb = WindowBatch(np.arange(n + 1, dtype=np.int32), ins, np.stack([tgt, neg], axis=1).astype(np.int32))
+    src = DeviceModel.from_host(P.EmbeddingModel(m_in, m_out))
+    dst = src.clone()
+    P.update_windows(dst, DeviceWindowBatch(wb), 1.0, src=src)
+    got = dst.to_host().output_vectors
+    e_tgt = got[tgt, 1]
+    e_neg = got[neg, 1]
+    exp_tgt = (1.0 - sig.astype(np.float64)).astype(np.float32)
+    bad_t = np.flatnonzero(e_tgt.view(np.uint32) != exp_tgt.view(np.uint32))
+    bad_n = np.flatnonzero(e_neg.view(np.uint32) != (-sig).view(np.uint32))
+    assert bad_t.size == 0, [(float(xs[i]), float(e_tgt[i]), float(exp_tgt[i])) for i in bad_t[:5]]
+    assert bad_n.size == 0, [(float(xs[i]), float(e_neg[i]), float(-sig[i])) for i in bad_n[:5]]

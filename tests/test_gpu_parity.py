@@ -51,7 +51,7 @@ def test_library_is_the_one_loaded():
     L = _lib.lib()
     maps = open("/proc/self/maps").read()
     assert _lib.LIB_PATH in maps
-    assert L.sgns_abi_version() == 1
+    assert L.sgns_abi_version() == 2
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
@@ -202,21 +202,20 @@ def test_snapshot_conflicting_windows(dtype, D, k):
     P.update_windows(dst, DeviceWindowBatch(wb), torch.from_numpy(alphas), src=src)
     got = dst.to_host()
     tab = SIGMOID_TABLE_F64 if dtype == "f64" else SIGMOID_TABLE_F32
-    acc_in = base.input_vectors.astype(np.float64).copy()
-    acc_out = base.output_vectors.astype(np.float64).copy()
-    for (a, b), al in zip(wins, alphas):
-        mi, mo = base.input_vectors.copy(), base.output_vectors.copy()
-        O.process_batch(mi, mo, a, b, float(npdt(al)), tab)
-        acc_in += mi.astype(np.float64) - base.input_vectors
-        acc_out += mo.astype(np.float64) - base.output_vectors
+    from oracle import pin
+    (acc_in, acc_out), mags, allows, _ = pin.snapshot_expectation(
+        base.input_vectors, base.output_vectors, wins, alphas, tab, check_edges=dtype == "f32")
     if dtype == "f64":
         np.testing.assert_allclose(got.input_vectors, acc_in, rtol=1e-10, atol=1e-13)
         np.testing.assert_allclose(got.output_vectors, acc_out, rtol=1e-10, atol=1e-13)
     else:
-        # float32 adds arrive in a different order (atomics): per-entry error scales with the
-        # number of contributions; bound it by 1e-5 relative to the summed |delta| magnitude
-        np.testing.assert_allclose(got.input_vectors, acc_in, rtol=1e-4, atol=2e-6)
-        np.testing.assert_allclose(got.output_vectors, acc_out, rtol=1e-4, atol=2e-6)
+        # float32 adds arrive in an unspecified order (atomics, per-warp hot-row sums), so the
+        # bound is 1e-5 relative to the magnitude summed, |snapshot| + sum_w |delta_w|, plus
+        # 1e-7, plus the table step of each cell whose score sits at a sigma-bin edge
+        for got_m, acc, mag, allow in zip((got.input_vectors, got.output_vectors), (acc_in, acc_out),
+                                         mags, allows):
+            worst = pin.snapshot_budget(got_m, acc, mag, allow)
+            assert worst <= 1.0, f"tolerance budget used {worst:.3f}"
 
 
 def _run_driver(ids, off, counts, *, window, k, cap, dynamic, subsample, seed, stream_base,

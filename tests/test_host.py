@@ -25,7 +25,7 @@ def test_library_exports_every_header_symbol():
     L = _lib.lib()
     for sym in declared:
         assert getattr(L, sym) is not None
-    assert L.sgns_abi_version() == 1
+    assert L.sgns_abi_version() == 2
     assert L.sgns_error_string(-3).decode().startswith("per-warp")
 
 

@@ -36,6 +36,17 @@ def test_writer_bytes_match_reference(tmp_path, binary):
     assert not back.output_vectors.any()
 
 
+@pytest.mark.parametrize("binary", [False, True])
+def test_writer_float64_bytes_match_reference(tmp_path, binary):
+    """A float64 model: text formats the float64 value itself (the reference's f"{v:.6g}"
+    of model.input_vectors[i]), binary casts to float32 -- both byte-identical."""
+    g, _, voc = _fixture()
+    v64 = g["vecs64"]
+    path = str(tmp_path / "v64")
+    save_model(EmbeddingModel(v64, np.zeros_like(v64)), voc, path, binary=binary)
+    assert open(path, "rb").read() == g[f"bytes64_{int(binary)}"].tobytes()
+
+
 def test_errors_and_debug_roundtrip(tmp_path):
     g, model, voc = _fixture()
     bad = tmp_path / "bad"
@@ -66,3 +77,9 @@ def test_device_rows_stream_to_same_bytes(tmp_path):
         path = str(tmp_path / f"d{int(binary)}")
         save_model(dm, voc, path, binary=binary)
         assert open(path, "rb").read() == g[f"bytes_{int(binary)}"].tobytes()
+    v64 = g["vecs64"]
+    dm64 = DeviceModel.from_host(EmbeddingModel(v64, np.zeros_like(v64)))
+    for binary in (False, True):
+        path = str(tmp_path / f"e{int(binary)}")
+        save_model(dm64, voc, path, binary=binary)
+        assert open(path, "rb").read() == g[f"bytes64_{int(binary)}"].tobytes()
