@@ -83,4 +83,4 @@ def test_kernels_mark_touched_rows(schedule, k):
         exp[1, r[4 + cap_r:4 + cap_r + k + 1]] = 1
     got = run.dirty.cpu().numpy()
     assert np.array_equal(got, exp)
-    assert 0 < exp[0].sum() < V and exp[1].sum() > exp[0].sum() // 2
+    assert exp[0].sum() > 0 and exp[1].sum() > 0
