@@ -164,8 +164,8 @@ def update_windows(dst: DeviceModel, batch: DeviceWindowBatch, alpha, *, src: De
 def process_batch(model, batch: Minibatch, alpha: float, matmul: str | None = None) -> None:
     """Apply one minibatch update in place on the GPU.
 
-    model: EmbeddingModel (host arrays, updated in place through a device
-    round trip) or DeviceModel (updated in HBM).  float64 models use the exact
+    model: EmbeddingModel (host arrays: only the window's distinct rows are copied
+    to the device and back, see _process_rows) or DeviceModel (updated in HBM).  float64 models use the exact
     sigmoid, float32 models the 1000-bin table, as the reference does.
     """
     if alpha < 0:
@@ -182,6 +182,32 @@ def process_batch(model, batch: Minibatch, alpha: float, matmul: str | None = No
     if not isinstance(model, EmbeddingModel):
         raise TypeError("model must be an EmbeddingModel or DeviceModel")
     wb.validate(model.vocab_size)
-    dm = DeviceModel.from_host(model)
-    update_windows(dm, DeviceWindowBatch(wb, dm.m_in.device), alpha)
-    dm.copy_to_host(model)
+    _process_rows(model, wb, alpha)
+
+
+def _process_rows(model: EmbeddingModel, wb: WindowBatch, alpha: float) -> None:
+    """Host model, row-granular: only the window's distinct input and output rows travel.
+
+    The reference's batch core gathers exactly these rows, updates them and scatters
+    them back (kernel_batched.py:92-144, :214-260).  Here the distinct rows of each
+    matrix are packed into a compact device model (ids remapped; repeated ids map to
+    one compact row, so repeated inputs accumulate into one row exactly as in place),
+    the launch runs on it, and the rows are written back -- (m + K + 1) rows each way
+    instead of the whole V x D model."""
+    import torch
+    in_rows, in_map = np.unique(wb.in_ids, return_inverse=True)
+    out_rows, out_map = np.unique(wb.out_ids, return_inverse=True)
+    n = max(len(in_rows), len(out_rows))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dm = DeviceModel.empty(n, model.dim, model.dtype, dev)
+    a = np.zeros((n, model.dim), dtype=model.dtype)
+    c = np.zeros((n, model.dim), dtype=model.dtype)
+    a[:len(in_rows)] = model.input_vectors[in_rows]
+    c[:len(out_rows)] = model.output_vectors[out_rows]
+    dm.m_in[:, :model.dim].copy_(torch.from_numpy(a))
+    dm.m_out[:, :model.dim].copy_(torch.from_numpy(c))
+    compact = WindowBatch(wb.in_off, in_map.astype(np.int32).reshape(wb.in_ids.shape),
+                          out_map.astype(np.int32).reshape(wb.out_ids.shape))
+    update_windows(dm, DeviceWindowBatch(compact, dev), alpha)
+    model.input_vectors[in_rows] = dm.m_in[:len(in_rows), :model.dim].cpu().numpy()
+    model.output_vectors[out_rows] = dm.m_out[:len(out_rows), :model.dim].cpu().numpy()

@@ -89,6 +89,49 @@ def test_process_batch_golden(dtype):
     assert worst <= 1.0, f"float32 tolerance budget used {worst:.2f}"
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_process_batch_host_row_granular(dtype, monkeypatch):
+    """Host models move only the window's distinct rows (kernel_batched.py:214-260 gathers
+    and scatters just those): repeated inputs, an input equal to an output id, V = 200k;
+    the result equals the oracle's in-place update and the device model allocated is
+    (distinct rows) x D, not V x D."""
+    P, O = _pkg(), _oracle()
+    from paper_1604_04661_b200 import model as M
+    from paper_1604_04661_b200.model import SIGMOID_TABLE_F32, SIGMOID_TABLE_F64
+    rng = np.random.default_rng(3)
+    V, D = 200_000, 96
+    a = (rng.normal(size=(V, D)) * 0.1).astype(dtype)
+    c = (rng.normal(size=(V, D)) * 0.1).astype(dtype)
+    ins = np.array([7, 199_999, 7, 42, 5, 7], np.int32)
+    outs = np.array([42, 0, 199_998, 5, 12], np.int32)
+    sizes = []
+    orig = M.DeviceModel.empty.__func__
+
+    def spy(cls, vocab_size, dim, dtype=np.float32, device="cuda"):
+        sizes.append(vocab_size)
+        return orig(cls, vocab_size, dim, dtype, device)
+    monkeypatch.setattr(M.DeviceModel, "empty", classmethod(spy))
+    model = P.EmbeddingModel(a.copy(), c.copy())
+    P.process_batch(model, P.Minibatch(ins, outs), 0.05)
+    assert sizes and max(sizes) <= len(ins) + len(outs), sizes
+    ra, rc = a.copy(), c.copy()
+    tab = SIGMOID_TABLE_F64 if dtype == np.float64 else SIGMOID_TABLE_F32
+    O.process_batch(ra, rc, ins, outs, 0.05, tab)
+    if dtype == np.float64:
+        np.testing.assert_allclose(model.input_vectors, ra, rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(model.output_vectors, rc, rtol=1e-12, atol=1e-15)
+    else:
+        assert not near_bin_edge(a[ins].astype(np.float64) @ c[outs].astype(np.float64).T).any()
+        assert f32_close(model.input_vectors, ra) <= 1.0
+        assert f32_close(model.output_vectors, rc) <= 1.0
+    touched_in = np.zeros(V, bool)
+    touched_in[ins] = True
+    touched_out = np.zeros(V, bool)
+    touched_out[outs] = True
+    assert np.array_equal(model.input_vectors[~touched_in], a[~touched_in])
+    assert np.array_equal(model.output_vectors[~touched_out], c[~touched_out])
+
+
 def test_process_batch_validation():
     P = _pkg()
     m = P.EmbeddingModel(np.zeros((5, 4), np.float32), np.zeros((5, 4), np.float32))

@@ -2,9 +2,10 @@
 and --impl reference arm time on the GPU box) against the real reference package
 (numba + OpenBLAS, /root/reference/pkg/src) on the same corpus, config and host cores.
 
-Runs in the build container only (the reference does not travel to the GPU box):
+The reference is imported from /root/reference/pkg/src in the build container and from
+baseline/_ref (its unmodified pip install, git-ignored, travels with gpurun) on the GPU box:
 
-    OPENBLAS_NUM_THREADS=1 python tools/calibrate_port.py > profiles/round1_port_calibration.json
+    OPENBLAS_NUM_THREADS=1 python tools/calibrate_port.py > profiles/round2_port_calibration_gpubox.json
 
 The port runs twice, with its batch_core_naive restatement (bit-exact pins) and its
 batch_core_blas restatement (the reference's default float32 backend; bench.py's CPU
@@ -22,7 +23,10 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, "/root/reference/pkg/src")
+REF_SRC = "/root/reference/pkg/src"
+if not os.path.isdir(REF_SRC):
+    REF_SRC = os.path.join(ROOT, "baseline", "_ref")  # pip install --target of the same package
+sys.path.insert(0, REF_SRC)
 
 
 def main(tokens=3_000_000, dim=300, seed=1):
@@ -72,7 +76,8 @@ def main(tokens=3_000_000, dim=300, seed=1):
                      "over_reference": trained / wall / ref["words_per_sec"]}
     print(json.dumps({
         "what": "oracle port (naive and blas cores) vs the reference package (its default float32 "
-                "backend, blas), same corpus/config/cores, build container",
+                "backend, blas), same corpus/config/cores",
+        "host": os.uname().nodename, "reference_from": REF_SRC,
         "corpus": f"{e.n_tokens} tokens Zipf(1.05) over {V} ids (planted clusters), d={dim} w=5 K=5 "
                   "t=1e-4, 1 epoch, float32",
         "threads": T, "cpu": _cpu_model(), "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS"),
