@@ -84,88 +84,102 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """SM clock and throttle reasons sampled during the timed region: NVML every 5 ms from
-    a background thread (the main thread sits in CUDA synchronisation), else nvidia-smi
-    every 50 ms.  LOCAL_RANK's device index is the NVML index (one process per GPU)."""
+    """SM clock and throttle reasons sampled during the timed region, from a separate
+    process (NVML every 2 ms, else nvidia-smi every 20 ms) so that this process's GIL,
+    held around CUDA synchronisation, cannot starve it.  Every sample carries a host
+    timestamp; stop() keeps those inside [mark_start(), mark_stop()].  LOCAL_RANK's
+    device index is the NVML index (one process per GPU)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    CHILD = r"""
+import sys, time
+import pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+        nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+out = open(sys.argv[2], "w", buffering=1)
+print("ready", flush=True)
+while True:
+    try:
+        t = time.time()
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        out.write("%.6f %d %d %s\n" % (t, sm, mx, ",".join(str(int(bool(r & b))) for b in bits)))
+    except Exception:
+        pass
+    time.sleep(0.002)
+"""
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.thread = None
-        self.sm, self.smax, self.reasons = [], [], set()
-
-    def _nvml_loop(self, nv, handle, bits):
-        import time as _t
-        while not self.stop_flag:
-            try:
-                self.sm.append(float(nv.nvmlDeviceGetClockInfo(handle, nv.NVML_CLOCK_SM)))
-                self.smax.append(float(nv.nvmlDeviceGetMaxClockInfo(handle, nv.NVML_CLOCK_SM)))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(handle)
-                for name, bit in zip(self.NAMES, bits):
-                    if r & bit:
-                        self.reasons.add(name)
-            except Exception:  # noqa: BLE001 - a failed sample is skipped
-                pass
-            _t.sleep(0.005)
+        self.path = tempfile.mktemp(suffix=".clk")
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
-            import threading
-            import pynvml as nv
-            nv.nvmlInit()
-            handle = nv.nvmlDeviceGetHandleByIndex(self.index)
-            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
-                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
-            self.stop_flag = False
-            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, handle, bits), daemon=True)
-            self.thread.start()
-            self.source = "nvml 5 ms"
+            self.proc = subprocess.Popen([sys.executable, "-c", self.CHILD, str(self.index), self.path],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            if self.proc.stdout.readline().strip() != "ready":
+                raise OSError("nvml sampler did not start")
+            self.source = "nvml 2 ms (sampler process)"
             return
-        except Exception:  # noqa: BLE001 - fall back to nvidia-smi
-            self.thread = None
+        except OSError:
+            if self.proc is not None:
+                self.proc.kill()
+            self.proc = None
         try:
-            self.path = tempfile.mktemp(suffix=".csv")
-            self.fh = open(self.path, "w")
+            self.fh = open(self.path + ".smi", "w")
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.fh,
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu=timestamp,{self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=self.fh,
                 stderr=subprocess.DEVNULL)
-            self.source = "nvidia-smi 50 ms"
+            self.source = "nvidia-smi 20 ms"
         except OSError:
             self.proc = None
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_stop(self):
+        self.t1 = time.time()
+
     def stop(self):
-        if self.thread is not None:
-            self.stop_flag = True
-            self.thread.join()
-        elif self.proc is not None:
-            self.proc.terminate()
-            self.proc.wait()
-            self.fh.close()
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        time.sleep(0.01)
+        self.proc.terminate()
+        self.proc.wait()
+        samples = []  # (t, sm, smax, [4 reason flags])
+        if self.source.startswith("nvml"):
             with open(self.path) as fh:
                 for line in fh:
-                    f = [x.strip() for x in line.split(",")]
-                    if len(f) < 6:
-                        continue
-                    try:
-                        self.sm.append(float(f[0]))
-                        self.smax.append(float(f[1]))
-                    except ValueError:
-                        continue
-                    for n, v in zip(self.NAMES, f[2:6]):
-                        if v.lower() == "active":
-                            self.reasons.add(n)
+                    f = line.split()
+                    if len(f) == 4:
+                        samples.append((float(f[0]), float(f[1]), float(f[2]), [x == "1" for x in f[3].split(",")]))
             os.unlink(self.path)
         else:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
-        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None,
-                "sm_max_mhz": float(max(self.smax)) if self.smax else None,
-                "samples": len(self.sm), "source": self.source, "reasons": sorted(self.reasons)}
+            import datetime
+            self.fh.close()
+            with open(self.path + ".smi") as fh:
+                for line in fh:
+                    f = [x.strip() for x in line.split(",")]
+                    try:
+                        t = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                        samples.append((t, float(f[1]), float(f[2]), [v.lower() == "active" for v in f[3:7]]))
+                    except (ValueError, IndexError):
+                        continue
+            os.unlink(self.path + ".smi")
+        inside = [x for x in samples if self.t0 is None or self.t0 <= x[0] <= (self.t1 or x[0])]
+        reasons = sorted({n for x in inside for n, on in zip(self.NAMES, x[3]) if on})
+        return {"sm_mhz": float(np.median([x[1] for x in inside])) if inside else None,
+                "sm_max_mhz": float(max(x[2] for x in inside)) if inside else None,
+                "samples": len(inside), "source": self.source, "reasons": reasons}
 
 
 def build_corpus(args, device):
@@ -468,23 +482,25 @@ def main():
             transport.allreduce_average(model.m_in, rows, "in")
             transport.allreduce_average(model.m_out, rows, "out")
 
+    clocks = ClockSampler(local)
+    clocks.start()  # a separate process: started before the warm-up, read over the timed region
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     c0 = counters()
-    clocks = ClockSampler(local)
-    clocks.start()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+    clocks.mark_start()
     t_start.record(stream)
     for i in range(args.steps):
         step(i)
     t_end.record(stream)
     torch.cuda.synchronize(dev)
+    clocks.mark_stop()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -519,8 +535,17 @@ def main():
                 "mean_inputs_per_chunk": my[2] / max(my[3], 1.0)}
     traffic_path = os.path.join(ROOT, "profiles", "drive_kernel_traffic.json")
     if os.path.exists(traffic_path):
+        # only a capture of this very kernel source counts (tools/ncu_traffic.py stamps it)
+        from tools.ncu_traffic import kernel_source_hash
         with open(traffic_path) as fh:
-            roofline["traffic"] = json.load(fh).get("dram_bytes_per_launch")
+            cap = json.load(fh)
+        if cap.get("kernel_src_sha") == kernel_source_hash():
+            roofline["traffic"] = cap.get("dram_bytes_per_launch")
+            roofline["traffic_capture"] = {"commit": cap.get("captured_at_commit"),
+                                           "kernel_src_sha": cap.get("kernel_src_sha")}
+        else:
+            roofline["traffic_note"] = (f"stale ncu capture (kernel sources changed since "
+                                        f"{cap.get('captured_at_commit')}): not reported")
         if roofline["traffic"]:
             # the same launch time against the DRAM bytes ncu measured: what HBM actually
             # moved (hot rows hit in L2, so this is well below the algorithmic figure)

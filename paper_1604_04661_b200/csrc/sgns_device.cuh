@@ -78,13 +78,6 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-// Same copy without the compiler memory clobber: for issue points that are already ordered
-// against the surrounding shared-memory accesses by __syncwarp() (a clobber there would
-// force every live shared value to be reloaded).
-__device__ __forceinline__ void cp_async16_nc(void *smem, const void *gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }

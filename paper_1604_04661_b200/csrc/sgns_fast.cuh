@@ -171,9 +171,6 @@ __device__ __forceinline__ void select_negatives(const FastArgs &p, NegCand cnd,
 #ifndef SGNS_FAST_MAXNREG
 #define SGNS_FAST_MAXNREG 128
 #endif
-#ifndef SGNS_FAST_EARLY_A
-#define SGNS_FAST_EARLY_A 1
-#endif
 #ifndef SGNS_FAST_MAXNREG_WIDE
 #define SGNS_FAST_MAXNREG_WIDE 168
 #endif
@@ -339,23 +336,19 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
       }
     }
     bool have = true;
-    bool a_issued = false;  // u's A rows already issued during the previous unit's dC pass
     while (have) {
       int *ids_s = ids_b + cur * idsn;
       const uint32_t *off_s = roff_b + cur * idsn;
       int *ids_n = ids_b + (cur ^ 1) * idsn;
       uint32_t *off_n = roff_b + (cur ^ 1) * idsn;
       const int m = u.mc;
-      // A rows of u -> smem (the first unit of a sentence; later units' rows were issued
-      // column block by column block inside the previous unit's dC pass)
-      if (!a_issued) {
-        for (int r = 0; r < m; ++r) {
-          const float *src = in_src_l + off_s[r];
-          float *dst = rows_s + r * ld + 4 * lane;
+      // A rows of u -> smem
+      for (int r = 0; r < m; ++r) {
+        const float *src = in_src_l + off_s[r];
+        float *dst = rows_s + r * ld + 4 * lane;
 #pragma unroll
-          for (int j = 0; j < NCH; ++j)
-            if (chunk_ok(j)) cp_async16(dst + 128 * j, src + 128 * j);
-        }
+        for (int j = 0; j < NCH; ++j)
+          if (chunk_ok(j)) cp_async16(dst + 128 * j, src + 128 * j);
       }
       if (p.dirty != nullptr) {  // touched rows (data-parallel touched-row averaging)
         for (int r = lane; r < m + k1; r += 32) p.dirty[(r < m ? 0u : p.vocab) + (uint32_t)ids_s[r]] = 1;
@@ -492,38 +485,22 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
       for (int k = 0; k < K1R; ++k) orow[k] = off_s[m + (kk_ok(k) ? k : 0)];
 #pragma unroll
       for (int j = 0; j < NS; ++j) {
-        const bool sj = slot_ok(j);  // false only on the tail lanes of a partial last slot
+        if (!slot_ok(j)) continue;
         const int col = 2 * (lane + 32 * j);
         float2 acc[K1R];
 #pragma unroll
         for (int k = 0; k < K1R; ++k) acc[k] = f2zero();
-        if (sj) {
-          const float *ap = rows_s + col;
-          const float *ep = e_s;
-          for (int i = 0; i < m; ++i, ap += ld, ep += 8) {
-            const float2 a0 = *reinterpret_cast<const float2 *>(ap);
-            const float4 e03 = *reinterpret_cast<const float4 *>(ep);
-            const float4 e47 = *reinterpret_cast<const float4 *>(ep + 4);
-            const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
+        const float *ap = rows_s + col;
+        const float *ep = e_s;
+        for (int i = 0; i < m; ++i, ap += ld, ep += 8) {
+          const float2 a0 = *reinterpret_cast<const float2 *>(ap);
+          const float4 e03 = *reinterpret_cast<const float4 *>(ep);
+          const float4 e47 = *reinterpret_cast<const float4 *>(ep + 4);
+          const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
 #pragma unroll
-            for (int k = 0; k < K1R; ++k)
-              if (kk_ok(k)) acc[k] = __ffma2_rn(make_float2(ev[k], ev[k]), a0, acc[k]);
-          }
+          for (int k = 0; k < K1R; ++k)
+            if (kk_ok(k)) acc[k] = __ffma2_rn(make_float2(ev[k], ev[k]), a0, acc[k]);
         }
-#if SGNS_FAST_EARLY_A
-        if (have) {
-          // slot j's columns (16-byte chunks [16 j, 16 j + 16)) of every staged row are dead
-          // now: gather u+1's rows into them.  u's dA scatters precede (same warp, ordered by
-          // the __syncwarp), so the copies read them, as a gather at u+1's start would.
-          __syncwarp();
-          const int mn = nx.mc;
-          for (int t = lane; t < 16 * mn; t += 32) {
-            const int r = t >> 4, cch = 16 * j + (t & 15);
-            if (cch < nvec) cp_async16_nc(rows_s + r * ld + 4 * cch, p.mv.in_src + off_n[r] + 4 * cch);
-          }
-        }
-#endif
-        if (!sj) continue;
 #pragma unroll
         for (int k = 0; k < K1R; ++k)
           if (kk_ok(k)) atomicAdd(reinterpret_cast<float2 *>(out_dst_l + orow[k] + 64 * j), acc[k]);
@@ -544,7 +521,6 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
         u = nx;
         cur ^= 1;
       }
-      a_issued = SGNS_FAST_EARLY_A != 0;
     }
   }
   // flush this worker's counters

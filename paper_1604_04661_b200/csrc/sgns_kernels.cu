@@ -11,20 +11,18 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
-#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "../../include/sgns_b200.h"
 #include "sgns_device.cuh"
 #include "sgns_fast.cuh"
-#include "sgns_ring.cuh"
 
-// The library is built from this one file as five translation units compiled in parallel
+// The library is built from this one file as four translation units compiled in parallel
 // (SGNS_PART 0: C ABI + init/slot kernels, 1: update_windows, 2: static driver, 3: fast
-// driver, 4: sentence-ring driver; see __graft_entry__.build_lib).  Without SGNS_PART it is
-// a single unit.  SGNS_ONLY_NS=n (experiment builds) instantiates the dynamic drivers for
-// one row width only.
+// driver; see __graft_entry__.build_lib).  Without SGNS_PART it is a single unit.
+// SGNS_ONLY_NS=n (experiment builds, tools/build_variant.py) instantiates the dynamic
+// driver for one row width only.
 #ifdef SGNS_PART
 #define SGNS_HAS(n) (SGNS_PART == (n))
 #else
@@ -582,18 +580,11 @@ static int prepare(K kernel, int64_t smem_bytes) {
   return e == cudaSuccess ? 0 : (int)e;
 }
 
-// Choose warps per block maximising resident warps for a given per-warp slab.  odd: also
-// try block sizes that are not powers of two (a slab that leaves room for 14 warps per SM
-// needs one 14-warp block: the per-block sigmoid table would not fit twice).
+// Choose warps per block maximising resident warps for a given per-warp slab.
 template <typename K>
-static int choose_wpb(K kernel, int64_t table, int64_t slab, int *wpb_out, int *blocks_per_sm,
-                      bool odd = false) {
+static int choose_wpb(K kernel, int64_t table, int64_t slab, int *wpb_out, int *blocks_per_sm) {
   int best = -1, best_w = 1, best_b = 1;
-  static const int pow2[] = {1, 2, 4, 8}, all[] = {1, 2, 4, 8, 10, 12, 13, 14, 15, 16};
-  const int *cand = odd ? all : pow2;
-  const int ncand = odd ? 10 : 4;
-  for (int ci = 0; ci < ncand; ++ci) {
-    const int w = cand[ci];
+  for (int w : {1, 2, 4, 8}) {
     const int64_t bytes = table + (int64_t)w * slab;
     if (bytes > 227 * 1024) break;
     if (prepare(kernel, bytes) != 0) break;
@@ -959,17 +950,6 @@ static int fast_ns(FastArgs a, int wpb, cudaStream_t st, int *res) {
               : launch_fast_t<NS, 6, false, false>(a, wpb, st, res);
 }
 
-int ring_dispatch(const FastArgs &a, int64_t ld, int wpb, cudaStream_t st, int *resident);
-
-// The sentence-ring driver (sgns_ring.cuh) runs when SGNS_FAST_KERNEL=ring and its ring fits
-// a warp's lanes (2 w + 2 <= 32); the default is the per-window-gather pipeline
-// (drive_fast_kernel), measured faster at d = 300.
-static bool use_ring(const sgns_drive_params *p) {
-  const char *e = std::getenv("SGNS_FAST_KERNEL");
-  if (e == nullptr || std::strcmp(e, "ring") != 0) return false;
-  return 2 * p->window + 2 <= 32;
-}
-
 int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
   FastArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -1014,7 +994,6 @@ int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
   a.loss_total = p->d_loss_total;
   a.dirty = p->d_dirty;
   const int wpb = p->warps_per_block;
-  if (use_ring(p)) return ring_dispatch(a, p->ld, wpb, st, resident);
   switch (ns_for(p->ld)) {
 #if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 1
     case 1: return fast_ns<1>(a, wpb, st, resident);
@@ -1046,78 +1025,6 @@ int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
 
 #endif  // SGNS_HAS(3)
 
-#if SGNS_HAS(4)
-// ------------------------------------------------------- sentence-ring path ----
-template <int NS, int K1R, bool EXACT, bool FULL>
-static int launch_ring_t(FastArgs a, int wpb_req, cudaStream_t st, int *resident) {
-  constexpr int NCH = (NS + 1) / 2;
-  auto kern = drive_ring_kernel<NS, NCH, K1R, EXACT, FULL>;
-  const RingSlab L = ring_slab(a.mv.ld, 2 * a.window + 2, std::min(a.cap, 2 * a.window), K1R, a.kept_cap);
-  int wpb = 0, bps = 0;
-  int rc = choose_wpb(kern, table_bytes(4), L.total, &wpb, &bps, true);
-  if (rc) return rc;
-  if (resident) {
-    *resident = wpb * bps * num_sms();
-    return 0;
-  }
-  if (wpb_req > 0) wpb = wpb_req;
-  a.wpb = wpb;
-  const int64_t bytes = table_bytes(4) + (int64_t)wpb * L.total;
-  if ((rc = prepare(kern, bytes))) return rc;
-  const int grid = (a.n_workers + wpb - 1) / wpb;
-  kern<<<grid, wpb * 32, bytes, st>>>(a);
-  return (int)cudaGetLastError();
-}
-
-template <int NS>
-static int ring_ns(const FastArgs &a, int64_t ld, int wpb, cudaStream_t st, int *res) {
-  const bool full = ld == 64 * NS;
-  switch (a.k_neg + 1) {
-    case 4: return full ? launch_ring_t<NS, 4, true, true>(a, wpb, st, res)
-                        : launch_ring_t<NS, 4, true, false>(a, wpb, st, res);
-    case 5: return full ? launch_ring_t<NS, 5, true, true>(a, wpb, st, res)
-                        : launch_ring_t<NS, 5, true, false>(a, wpb, st, res);
-    case 6: return full ? launch_ring_t<NS, 6, true, true>(a, wpb, st, res)
-                        : launch_ring_t<NS, 6, true, false>(a, wpb, st, res);
-    case 7: return full ? launch_ring_t<NS, 7, true, true>(a, wpb, st, res)
-                        : launch_ring_t<NS, 7, true, false>(a, wpb, st, res);
-    case 8: return full ? launch_ring_t<NS, 8, true, true>(a, wpb, st, res)
-                        : launch_ring_t<NS, 8, true, false>(a, wpb, st, res);
-  }
-  return full ? launch_ring_t<NS, 6, false, true>(a, wpb, st, res)
-              : launch_ring_t<NS, 6, false, false>(a, wpb, st, res);
-}
-
-int ring_dispatch(const FastArgs &a, int64_t ld, int wpb, cudaStream_t st, int *resident) {
-  switch (ns_for(ld)) {
-#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 1
-    case 1: return ring_ns<1>(a, ld, wpb, st, resident);
-#endif
-#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 2
-    case 2: return ring_ns<2>(a, ld, wpb, st, resident);
-#endif
-#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 3
-    case 3: return ring_ns<3>(a, ld, wpb, st, resident);
-#endif
-#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 4
-    case 4: return ring_ns<4>(a, ld, wpb, st, resident);
-#endif
-#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 5
-    case 5: return ring_ns<5>(a, ld, wpb, st, resident);
-#endif
-#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 6
-    case 6: return ring_ns<6>(a, ld, wpb, st, resident);
-#endif
-#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 7
-    case 7: return ring_ns<7>(a, ld, wpb, st, resident);
-#endif
-#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 8
-    case 8: return ring_ns<8>(a, ld, wpb, st, resident);
-#endif
-  }
-  return SGNS_E_SHAPE;
-}
-#endif  // SGNS_HAS(4)
 
 #if SGNS_HAS(0)
 static bool fast_eligible(const sgns_drive_params *p) {

@@ -1,5 +1,4 @@
-"""Pins the timed production kernels (drive_ring_kernel, csrc/sgns_ring.cuh, the default,
-and drive_fast_kernel, csrc/sgns_fast.cuh) at the
+"""Pins the timed production kernel (drive_fast_kernel, csrc/sgns_fast.cuh) at the
 north-star tolerance, window stream by window stream, and the device sigma-bin rule at
 the reference's 3,008 edge probes.
 
@@ -62,11 +61,6 @@ CASES = [(d, k, 16) for d in (100, 300, 512) for k in (3, 4, 5, 6, 7)]
 CASES += [(4, 5, 16), (4, 7, 16), (64, 2, 16), (320, 5, 16), (300, 5, 4), (100, 7, 4), (512, 3, 4)]
 
 
-# both dynamic-schedule kernels: the sentence ring (sgns_ring.cuh, the default for
-# w <= 15) and the per-window-gather pipeline (sgns_fast.cuh, SGNS_FAST_KERNEL=pipe)
-KERNELS = ["ring", "pipe"]
-
-
 def _pin_case(D, k, cap, window=5, V=12, n_sent=60, lo=4, hi=12, seed_extra=0):
     import paper_1604_04661_b200 as P
     from paper_1604_04661_b200.model import DeviceModel, SIGMOID_TABLE_F32
@@ -83,10 +77,8 @@ def _pin_case(D, k, cap, window=5, V=12, n_sent=60, lo=4, hi=12, seed_extra=0):
     return t
 
 
-@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("D,k,cap", CASES, ids=[f"d{d}_k{k}_cap{c}" for d, k, c in CASES])
-def test_fast_kernel_per_sentence_vs_oracle(D, k, cap, kernel, monkeypatch):
-    monkeypatch.setenv("SGNS_FAST_KERNEL", kernel)
+def test_fast_kernel_per_sentence_vs_oracle(D, k, cap):
     t = _pin_case(D, k, cap)
     assert t["windows"] > 200 and t["shared_next"] > t["windows"] // 2, t
     assert t["compared"] >= 0.7 * 60, t  # the rest hold a score at a sigma-bin edge
@@ -94,16 +86,15 @@ def test_fast_kernel_per_sentence_vs_oracle(D, k, cap, kernel, monkeypatch):
     assert t["worst"] <= 1.0, t
 
 
-# ring span R = 2w + 2: w = 1 (4 slots), 2, 10 (chunked: cap 16 < 2w), 15 (R = 32 lanes);
-# w = 16 runs the pipeline kernel (R would exceed a warp).  Long sentences (14..34 kept
-# positions) wrap the ring; V = 12 repeats words inside the span constantly
-# (the ring's slow path), V = 5000 almost never (its fast path).
+# window half-widths beyond the default: w = 1, 2, 10 (chunked: cap 16 < 2w), 15, 16 over
+# long sentences (14..34 positions); V = 12 repeats words inside every window, V = 5000
+# rarely.
 WCASES = [(300, 5, 16, w, V) for w in (1, 2, 10, 15, 16) for V in (12, 5000)]
 WCASES += [(100, 7, 4, 10, 12), (512, 3, 16, 5, 5000)]
 
 
 @pytest.mark.parametrize("D,k,cap,window,V", WCASES, ids=[f"d{d}_k{k}_cap{c}_w{w}_V{v}" for d, k, c, w, v in WCASES])
-def test_ring_kernel_windows_vs_oracle(D, k, cap, window, V):
+def test_fast_kernel_windows_vs_oracle(D, k, cap, window, V):
     t = _pin_case(D, k, cap, window=window, V=V, n_sent=60, lo=14, hi=34)
     assert t["windows"] > 300, t
     # long windows hold many scores, so more sentences meet a sigma-bin edge
