@@ -12,8 +12,8 @@ fused device driver, then (N > 1) the full model is averaged with NCCL.
 (oracle/, kind "port": splitmix stream, 10^8-slot negative table, the reference's
 default float32 batch_core_blas core, one pthread per host core, Hogwild) on the
 same corpus, config, metric and step definition, on rank 0 only.  On equal cores
-the port runs 1.67x the reference package's own speed
-(profiles/round1_port_calibration.json), so the GPU/CPU ratio is conservative.
+the port runs 1.36x the reference package's own speed on the GPU box's 16 host cores
+(profiles/round2_port_calibration_gpubox.json), so the GPU/CPU ratio is conservative.
 """
 
 from __future__ import annotations
@@ -60,6 +60,10 @@ def parse():
     ap.add_argument("--sync-hot-rows", type=int, default=-1,
                     help="configs[4] sweep: average only rows [0, N) + the reference's round-robin "
                          "chunk each step (-1: full model, configs[3])")
+    ap.add_argument("--sync-touched", action="store_true",
+                    help="average only the rows some rank wrote during the period (exact: untouched rows "
+                         "are equal on every replica); N=1 also reports the touched-row union over 1..8 "
+                         "periods, the volume such a sync moves")
     ap.add_argument("--sync-rotation", type=int, default=-1,
                     help="rotation chunk for --sync-hot-rows (-1: the reference default, 1/20 of the cold rows)")
     ap.add_argument("--config", choices=["large", "micro"], default="large",
@@ -244,8 +248,8 @@ def cpu_reference_run(corpus, enc, shard, args, seconds=None, steps=None, warmup
     return {"value": trained / el, "unit": UNIT, "cores": T, "kind": "port",
             "sample": f"{n} steps x {args.period} words read (= {read} read, {trained} trained) of the "
                       f"same corpus, splitmix + 1e8-slot table, batch_core_blas restatement (the "
-                      f"reference's default float32 core; 1.67x the reference package's own speed on "
-                      f"equal cores, profiles/round1_port_calibration.json), {T} pthreads, float32 "
+                      f"reference's default float32 core; 1.36x the reference package's own speed on "
+                      f"the GPU box's 16 cores, profiles/round2_port_calibration_gpubox.json), {T} pthreads, float32 "
                       f"model V={V} d={DIM}",
             "seconds": el, "steps": n}
 
@@ -276,8 +280,9 @@ def config_block(args, world):
             "tokens": args.tokens, "vocab_raw": args.vocab, "dim": DIM, "window": WINDOW,
             "negatives": NEG, "subsample": SUBSAMPLE, "period_words_per_gpu": args.period,
             "parallelism": f"dp{world}",
-            "sync": "full model every period" if args.sync_hot_rows < 0 else
-                    f"rows [0,{args.sync_hot_rows}) + round-robin chunk every period",
+            "sync": ("full model every period" if args.sync_hot_rows < 0 else
+                     f"rows [0,{args.sync_hot_rows}) + round-robin chunk every period")
+                    + (", only rows some rank wrote (touched-row average)" if args.sync_touched else ""),
             "l2": "model 2.4 GB and corpus 3.2 GB exceed the 126 MB L2; no flush between steps",
             **({"dist_backend": os.environ["SGNS_BENCH_DIST_BACKEND"] + " (plumbing check, not a measurement)"}
                if os.environ.get("SGNS_BENCH_DIST_BACKEND", "nccl") != "nccl" else {})}
@@ -445,7 +450,7 @@ def main():
     alpha0_eff = scaled_alpha0(ALPHA0, world)
     total_x = float(corpus.n_tokens) * epochs / world
     run = DeviceRun(model, dcorp, sampler, keep, cfg, alpha0_eff, total_x, W, sent_range=shard,
-                    stream_base=rank * W)
+                    stream_base=rank * W, track_dirty=args.sync_touched)
     transport = NcclTransport() if world > 1 else None
     budget = math.ceil(args.period / W)
     stream = torch.cuda.current_stream(dev)
@@ -479,8 +484,22 @@ def main():
             k_ev[i][1].record(stream)
         if transport is not None:
             rows = sync_rows()
-            transport.allreduce_average(model.m_in, rows, "in")
-            transport.allreduce_average(model.m_out, rows, "out")
+            if args.sync_touched:
+                sync_touched(rows)
+            else:
+                transport.average_rows(model, rows)  # one coalesced collective (NCCL group)
+
+    def sync_touched(rows):
+        from paper_1604_04661_b200.distributed import row_runs
+        transport.union_flags(run.dirty)
+        runs = row_runs(rows)
+        parts = []
+        for w, m in enumerate((model.m_in, model.m_out)):
+            idx = [torch.nonzero(run.dirty[w, lo:hi]).flatten() + lo for lo, hi in runs]
+            parts.append((m, torch.cat(idx)))
+        transport.average_packed(parts)
+        for lo, hi in runs:
+            run.dirty[:, lo:hi] = 0
 
     clocks = ClockSampler(local)
     clocks.start()  # a separate process: started before the warm-up, read over the timed region
@@ -552,6 +571,18 @@ def main():
             roofline["dram_achieved"] = roofline["traffic"] / avg_kernel_s / 1e9
             roofline["dram_frac"] = roofline["dram_achieved"] / peak
 
+    touched = None
+    if args.sync_touched and world == 1:
+        # rows written by one GPU's period, and the union over n consecutive periods: the
+        # union over n ranks' concurrent periods (statistically alike shards) is what an
+        # n-GPU touched-row sync averages
+        run.dirty.zero_()
+        touched = {"rows": V}
+        for n in range(1, 9):
+            run.launch(budget)
+            c = run.dirty.sum(dim=1, dtype=torch.int64).cpu().tolist()
+            touched[str(n)] = {"in": c[0], "out": c[1], "bytes": (c[0] + c[1]) * model.ld * 4}
+
     # ---- e2e: the public streaming API from pinned host buffers (H2D + D2H in the timed region)
     e2e = None
     if not args.no_e2e:
@@ -572,7 +603,7 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": config_block(args, world), "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": args.steps, "clocks": clk,
-                "words_read_per_sec": read / (max_ms / 1000.0),
+                "words_read_per_sec": read / (max_ms / 1000.0), "touched_rows_by_periods": touched,
                 "workers_per_gpu": W, "corpus_gen_seconds": t_gen}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -610,9 +641,7 @@ def e2e_leg(args, corpus, enc, shard, cfg, counts, keep, world, rank, dev, alpha
     stream = torch.cuda.current_stream(dev)
 
     def sync():
-        rows = sync_rows()
-        transport.allreduce_average(model.m_in, rows, "in")
-        transport.allreduce_average(model.m_out, rows, "out")
+        transport.average_rows(model, sync_rows())  # one coalesced collective
     after = sync if transport is not None else None
 
     off_pinned = torch.from_numpy(np.ascontiguousarray(off, dtype=np.int64)).pin_memory()

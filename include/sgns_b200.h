@@ -41,7 +41,8 @@ enum {
   SGNS_E_SMEM = -3,      /* per-warp staging does not fit in shared memory */
   SGNS_E_DEVICE = -4,    /* device-side validation failed (see sgns_error_string) */
   SGNS_E_IO = -5,        /* corpus file could not be opened / mapped */
-  SGNS_E_EMPTY = -6      /* no token reaches min_count (EmptyVocabularyError) */
+  SGNS_E_EMPTY = -6,     /* no token reaches min_count (EmptyVocabularyError) */
+  SGNS_E_TRUNC = -7      /* vector file ends inside a row (ModelFormatError "truncated") */
 };
 
 enum { SGNS_F32 = 0, SGNS_F64 = 1 };
@@ -182,6 +183,19 @@ void sgns_encoded_free(sgns_encoded *e);
 int sgns_write_vectors(const char *path, const char *tokens_blob, const int64_t *token_offsets,
                        int64_t vocab, int32_t dim, const void *rows, int64_t ld, int32_t binary,
                        int32_t rows_on_device, int32_t dtype);
+
+/* Vector-file reader (replaces the parsing in load_model / detect_format,
+ * sgns/model.py:140-225).  Status 1 = "this item needs Python's own rules" (a header or
+ * row outside the plain-ASCII fast path); the caller handles it and resumes.
+ *   sgns_vectors_header: "V D" of the first line; *header_bytes = its length with '\n'.
+ *   sgns_vectors_sniff:  detect_format's decision (*binary = 1 / 0).
+ *   sgns_parse_vectors:  rows [*row, vocab) from byte *offset: vectors (vocab x dim
+ *                        float32), token byte spans; on return *row / *offset say where
+ *                        it stopped (status 1 or SGNS_E_TRUNC) or vocab / end (SGNS_OK). */
+int sgns_vectors_header(const char *path, int64_t *vocab, int32_t *dim, int64_t *header_bytes);
+int sgns_vectors_sniff(const char *path, int64_t header_bytes, int32_t dim, int32_t *binary);
+int sgns_parse_vectors(const char *path, int32_t binary, int64_t vocab, int32_t dim, float *vectors,
+                       int64_t *tok_start, int64_t *tok_end, int64_t *row, int64_t *offset);
 
 const char *sgns_error_string(int32_t code);
 int sgns_abi_version(void);

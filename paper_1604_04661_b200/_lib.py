@@ -97,6 +97,12 @@ def lib() -> C.CDLL:
     L.sgns_encoded_free.argtypes = [P]
     L.sgns_write_vectors.restype = C.c_int
     L.sgns_write_vectors.argtypes = [C.c_char_p, P, P, I64, I32, P, I64, I32, I32, I32]
+    L.sgns_vectors_header.restype = C.c_int
+    L.sgns_vectors_header.argtypes = [C.c_char_p, C.POINTER(I64), C.POINTER(I32), C.POINTER(I64)]
+    L.sgns_vectors_sniff.restype = C.c_int
+    L.sgns_vectors_sniff.argtypes = [C.c_char_p, I64, I32, C.POINTER(I32)]
+    L.sgns_parse_vectors.restype = C.c_int
+    L.sgns_parse_vectors.argtypes = [C.c_char_p, I32, I64, I32, P, P, P, C.POINTER(I64), C.POINTER(I64)]
     L.sgns_struct_sizes.restype = C.c_int
     L.sgns_struct_sizes.argtypes = [C.POINTER(I32), C.POINTER(I32)]
     if L.sgns_abi_version() != 2:
@@ -114,7 +120,7 @@ EXPORTED = ("sgns_update_windows", "sgns_drive", "sgns_init_model", "sgns_expand
             "sgns_build_alias", "sgns_resident_workers", "sgns_error_string", "sgns_abi_version",
             "sgns_struct_sizes", "sgns_vocab_build", "sgns_vocab_from_tokens", "sgns_vocab_export",
             "sgns_vocab_free", "sgns_encode", "sgns_encoded_export", "sgns_encoded_free",
-            "sgns_write_vectors")
+            "sgns_write_vectors", "sgns_vectors_header", "sgns_vectors_sniff", "sgns_parse_vectors")
 
 
 class SgnsError(RuntimeError):

@@ -26,24 +26,11 @@
 #include <vector>
 
 #include "../../include/sgns_b200.h"
+#include "sgns_text.hpp"
 
 namespace {
 
-// length of the whitespace code point starting at p (0: not whitespace)
-inline int ws_len(const unsigned char *p, const unsigned char *end) {
-  const unsigned char c = p[0];
-  if (c == ' ' || (c >= 0x09 && c <= 0x0d) || (c >= 0x1c && c <= 0x1f)) return 1;
-  if (c < 0xc2) return 0;
-  if (c == 0xc2 && p + 1 < end && (p[1] == 0x85 || p[1] == 0xa0)) return 2;
-  if (c == 0xe1 && p + 2 < end && p[1] == 0x9a && p[2] == 0x80) return 3;
-  if (c == 0xe2 && p + 2 < end) {
-    if (p[1] == 0x80 && ((p[2] >= 0x80 && p[2] <= 0x8a) || p[2] == 0xa8 || p[2] == 0xa9 || p[2] == 0xaf))
-      return 3;
-    if (p[1] == 0x81 && p[2] == 0x9f) return 3;
-  }
-  if (c == 0xe3 && p + 2 < end && p[1] == 0x80 && p[2] == 0x80) return 3;
-  return 0;
-}
+using sgns_text::ws_len;
 
 struct Mapped {
   const unsigned char *data = nullptr;

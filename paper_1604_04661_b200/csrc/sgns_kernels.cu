@@ -1075,6 +1075,7 @@ const char *sgns_error_string(int32_t code) {
     case SGNS_E_DEVICE: return "device-side validation failed";
     case SGNS_E_IO: return "corpus file could not be opened";
     case SGNS_E_EMPTY: return "no token appears at least min_count times";
+    case SGNS_E_TRUNC: return "vector file ends inside a row";
   }
   if (code > 0) return cudaGetErrorString((cudaError_t)code);
   return "unknown error";

@@ -235,75 +235,107 @@ def save_model(model, vocab, path: str, binary: bool = False) -> None:
     _lib.check(rc, "sgns_write_vectors")
 
 
-def _parse_header(line: bytes, path: str) -> tuple[int, int]:
+def _header(path: str) -> tuple[int, int, int]:
+    """(V, D, header length in bytes): the native parser, else Python's int()/split() rules
+    for the first line (sgns/model.py:140-150 semantics)."""
+    import ctypes as C
+    v, d, n = C.c_int64(0), C.c_int32(0), C.c_int64(0)
+    rc = _lib.lib().sgns_vectors_header(path.encode(), C.byref(v), C.byref(d), C.byref(n))
+    if rc == -5:
+        raise FileNotFoundError(path)
+    if rc == 0:
+        return v.value, d.value, n.value
+    with open(path, "rb") as fh:
+        first = fh.readline()
+    bad = ModelFormatError(f"{path}: malformed header {first!r}")
     try:
-        fields = line.decode("utf-8").split()
-        if len(fields) != 2:
-            raise ValueError
-        v, d = int(fields[0]), int(fields[1])
-        if v < 1 or d < 1:
-            raise ValueError
-    except (ValueError, UnicodeDecodeError):
-        raise ModelFormatError(f"{path}: malformed header {line!r}") from None
-    return v, d
+        words = first.decode("utf-8").split()
+        dims = [int(x) for x in words] if len(words) == 2 else None
+    except (UnicodeDecodeError, ValueError):
+        dims = None
+    if not dims or min(dims) < 1:
+        raise bad from None
+    return dims[0], dims[1], len(first)
 
 
 def detect_format(path: str) -> bool:
-    """True when the payload looks binary (same sniffing rule as model.py:155-172)."""
+    """True when the payload looks binary: the first row, decoded and whitespace-split,
+    must hold a token and D numbers to count as text (sgns/model.py:153-172 rule)."""
+    import ctypes as C
+    _, d, hdr = _header(path)
+    out = C.c_int32(0)
+    rc = _lib.lib().sgns_vectors_sniff(path.encode(), hdr, d, C.byref(out))
+    if rc == 0:
+        return bool(out.value)
+    _lib.check(rc if rc < 0 else 0, "sgns_vectors_sniff")
+    with open(path, "rb") as fh:  # a probe field only Python's float() can judge
+        fh.seek(hdr)
+        fields = fh.read(16 * d + 64).decode("utf-8").split()
+    for f in fields[1:d + 1]:
+        try:
+            float(f)
+        except ValueError:
+            return True
+    return False
+
+
+def _python_row(path: str, binary: bool, offset: int, d: int, row: int, vocab: int):
+    """One row the native parser handed back, under Python's rules: (token, values, next
+    offset) or the exception the reference raises for it."""
     with open(path, "rb") as fh:
-        v, d = _parse_header(fh.readline(), path)
-        probe = fh.read(d * 16 + 64)
-    try:
-        text = probe.decode("utf-8")
-    except UnicodeDecodeError:
-        return True
-    fields = text.split()
-    if len(fields) < d + 1:
-        return len(probe) > 0
-    try:
-        [float(f) for f in fields[1:d + 1]]
-        return False
-    except ValueError:
-        return True
+        fh.seek(offset)
+        if binary:  # only an undecodable token comes back here
+            raw = fh.read()
+            return raw[:raw.index(b" ")].decode("utf-8"), None, None
+        raw = fh.read()
+    # Python text mode: universal newlines, the row ends at \n, \r\n or \r
+    cut = len(raw)
+    for sep in (b"\n", b"\r"):
+        k = raw.find(sep)
+        if 0 <= k < cut:
+            cut = k
+    nxt = offset + cut + (2 if raw[cut:cut + 2] == b"\r\n" else 1 if cut < len(raw) else 0)
+    line = raw[:cut].decode("utf-8")
+    cols = line.split(" ")
+    if len(cols) - 1 != d:
+        raise ModelFormatError(f"{path}: dimension mismatch at word {row}: expected {d} values, got {len(cols) - 1}")
+    return cols[0], np.array([float(x) for x in cols[1:]], dtype=np.float32), nxt
 
 
 def load_model(path: str, binary: bool | None = None):
-    """Read a vector file back (model.py:175-225); output_vectors come back zero."""
+    """Read a vector file back (sgns/model.py:175-225): rows parsed natively
+    (sgns_parse_vectors), output_vectors come back zero, counts are ones."""
+    import ctypes as C
     from .corpus import Vocabulary
+    v, d, hdr = _header(path)
     if binary is None:
         binary = detect_format(path)
-    tokens: list[str] = []
+    vectors = np.empty((v, d), dtype=np.float32)
+    t0 = np.zeros(v, dtype=np.int64)
+    t1 = np.zeros(v, dtype=np.int64)
+    names: dict[int, str] = {}  # rows that came back through _python_row
+    row, off = C.c_int64(0), C.c_int64(hdr)
+    L = _lib.lib()
+    while True:
+        rc = L.sgns_parse_vectors(path.encode(), int(binary), v, d, vectors.ctypes.data, t0.ctypes.data,
+                                  t1.ctypes.data, C.byref(row), C.byref(off))
+        if rc == 0:
+            break
+        if rc == -7:
+            raise ModelFormatError(f"{path}: truncated file at word {row.value} of {v}")
+        _lib.check(rc if rc < 0 else 0, "sgns_parse_vectors")
+        tok, vals, nxt = _python_row(path, binary, off.value, d, row.value, v)
+        names[row.value] = tok
+        vectors[row.value] = vals
+        row.value += 1
+        off.value = nxt
+    import mmap
+    with open(path, "rb") as fh, mmap.mmap(fh.fileno(), 0, access=mmap.ACCESS_READ) as blob:
+        tokens = [names[i] if i in names else blob[a:b].decode("utf-8")
+                  for i, (a, b) in enumerate(zip(t0.tolist(), t1.tolist()))]
     if binary:
-        with open(path, "rb") as fh:
-            v, d = _parse_header(fh.readline(), path)
-            data = fh.read()
-        vectors = np.empty((v, d), dtype=np.float32)
-        pos, nb = 0, 4 * d
-        for i in range(v):
-            sp = data.find(b" ", pos)
-            if sp < 0 or sp + 1 + nb > len(data):
-                raise ModelFormatError(f"{path}: truncated file at word {i} of {v}")
-            tokens.append(data[pos:sp].decode("utf-8").lstrip("\n"))
-            vectors[i] = np.frombuffer(data, dtype="<f4", count=d, offset=sp + 1)
-            pos = sp + 1 + nb
-            if pos < len(data) and data[pos:pos + 1] == b"\n":
-                pos += 1
-    else:
-        with open(path, encoding="utf-8") as fh:
-            v, d = _parse_header(fh.readline().encode("utf-8"), path)
-            vectors = np.empty((v, d), dtype=np.float32)
-            for i in range(v):
-                line = fh.readline()
-                if not line:
-                    raise ModelFormatError(f"{path}: truncated file at word {i} of {v}")
-                fields = line.rstrip("\n").split(" ")
-                if len(fields) != d + 1:
-                    raise ModelFormatError(f"{path}: dimension mismatch at word {i}: "
-                                           f"expected {d} values, got {len(fields) - 1}")
-                tokens.append(fields[0])
-                vectors[i] = [float(f) for f in fields[1:]]
-    counts = np.ones(v, dtype=np.int64)
-    vocab = Vocabulary(tokens, counts, {t: i for i, t in enumerate(tokens)}, v)
+        tokens = [t.lstrip("\n") for t in tokens]
+    vocab = Vocabulary(tokens, np.ones(v, dtype=np.int64), {t: i for i, t in enumerate(tokens)}, v)
     return EmbeddingModel(vectors, np.zeros_like(vectors)), vocab
 
 

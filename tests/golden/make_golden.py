@@ -399,11 +399,73 @@ def gen_io():
     np.savez_compressed(os.path.join(HERE, "io.npz"), **out)
 
 
+READ_CASES = [
+    # (name, file bytes, binary flag passed to load_model: None = detect_format)
+    ("plain", b"3 2\na 1 2\nb -0.5 3e-3\nc 1e10 -7\n", None),
+    ("py_numbers", b"3 3\nx +1.5 1_000.25 .5\ny 5. -.25e+2 1E-45\nz inf -Infinity nan\n", None),
+    ("crlf_and_cr", b"2 2\r\na 1 2\r\nb 3 4\rc 9 9\n", False),
+    ("tab_in_field", b"2 2\na \t1 2\nb 3 4\t\n", False),
+    ("fullwidth_digits", "2 2\nu \uff11.5 2\nv 3 \u0664\n".encode(), False),
+    ("utf8_tokens", "2 2\nnaïve 1 2\n日本語 3 4\n".encode(), None),
+    ("no_final_newline", b"2 2\na 1 2\nb 3 4", None),
+    ("dup_tokens", b"3 1\na 1\nb 2\na 3\n", None),
+    ("extra_field", b"2 2\na 1 2\nb 3 4 5\n", False),
+    ("missing_field", b"2 2\na 1\nb 3 4\n", False),
+    ("blank_line", b"2 2\na 1 2\n\nb 3 4\n", False),
+    ("double_space", b"2 2\na 1  2\nb 3 4\n", False),
+    ("bad_number", b"2 2\na 1 2\nb 3 x4\n", False),
+    ("truncated_text", b"3 2\na 1 2\nb 3 4\n", False),
+    ("bad_header", b"3 x\na 1 2\n", None),
+    ("header_three", b"3 2 1\na 1 2\n", None),
+    ("header_zero", b"0 2\n", None),
+    ("header_underscore", b"1_0 1\n" + b"".join(b"w%d %d\n" % (i, i) for i in range(10)), None),
+    ("bin_plain", b"2 2\n" + b"a " + np.array([1.5, -2], "<f4").tobytes() + b"\n" + b"bb "
+     + np.array([3, 4], "<f4").tobytes() + b"\n", None),
+    ("bin_no_newlines", b"2 1\n" + b"a " + np.array([1], "<f4").tobytes() + b"b "
+     + np.array([2], "<f4").tobytes(), True),
+    ("bin_leading_newline_token", b"2 1\n\na " + np.array([1], "<f4").tobytes() + b"\n\n\nb "
+     + np.array([2], "<f4").tobytes(), True),
+    ("bin_truncated_payload", b"2 2\na " + np.array([1, 2], "<f4").tobytes() + b"\nb \x00\x00", True),
+    ("bin_truncated_token", b"2 2\na " + np.array([1, 2], "<f4").tobytes() + b"\nbbb", True),
+    ("bin_bad_utf8", b"1 1\n\xff\xfe " + np.array([1], "<f4").tobytes() + b"\n", True),
+    ("bin_space_payload", b"2 1\n" + b"a " + np.array([np.float32(32.0 / 2 ** 126)], "<f4").tobytes()
+     + b"\nb " + np.array([8.0], "<f4").tobytes() + b"\n", True),
+    ("sniff_binary", b"2 2\n" + b"a " + np.array([1e-3, 7], "<f4").tobytes() + b"\nb "
+     + np.array([3, 4], "<f4").tobytes() + b"\n", None),
+    ("sniff_short_text", b"4 3\na 1\n", None),
+    ("sniff_empty_body", b"2 2\n", None),
+    ("text_bad_utf8", b"2 1\na 1\n\xc3 2\n", False),
+]
+
+
+def gen_read():
+    """The reference's load_model (and detect_format) outcome on every READ_CASES file:
+    tokens and float32 bits, or the exception class and message."""
+    out = {"names": np.array("\x00".join(c[0] for c in READ_CASES))}
+    for name, data, binary in READ_CASES:
+        path = os.path.join("/tmp", "golden_read_" + name)
+        with open(path, "wb") as fh:
+            fh.write(data)
+        out[f"{name}__bytes"] = np.frombuffer(data, dtype=np.uint8)
+        out[f"{name}__binary"] = np.array(-1 if binary is None else int(binary))
+        try:
+            model, voc = rm.load_model(path, binary)
+            out[f"{name}__tokens"] = np.array("\x00".join(voc.tokens))
+            out[f"{name}__vecs"] = model.input_vectors.view(np.uint32)
+        except Exception as exc:  # noqa: BLE001 -- the outcome is the fixture
+            out[f"{name}__error"] = np.array(type(exc).__name__ + ": " + str(exc).replace(path, "<path>"))
+        try:
+            out[f"{name}__sniff"] = np.array(int(rm.detect_format(path)))
+        except Exception as exc:  # noqa: BLE001
+            out[f"{name}__sniff_error"] = np.array(type(exc).__name__)
+    np.savez_compressed(os.path.join(HERE, "read.npz"), **out)
+
+
 if __name__ == "__main__":
     assert sgns.__version__
     only = set(sys.argv[1:])  # e.g. "gen_io": regenerate one fixture
     for fn in (gen_rng, gen_tables, gen_init, gen_kernel, gen_traces, gen_train, gen_dist, gen_eval,
-               gen_ingest, gen_io, gen_eval_full):
+               gen_ingest, gen_io, gen_eval_full, gen_read):
         if only and fn.__name__ not in only:
             continue
         fn()

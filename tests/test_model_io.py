@@ -83,3 +83,41 @@ def test_device_rows_stream_to_same_bytes(tmp_path):
         path = str(tmp_path / f"e{int(binary)}")
         save_model(dm64, voc, path, binary=binary)
         assert open(path, "rb").read() == g[f"bytes64_{int(binary)}"].tobytes()
+
+
+def _read_cases():
+    g = load_golden("read")
+    return g, str(g["names"]).split("\x00")
+
+
+@pytest.mark.parametrize("name", _read_cases()[1])
+def test_reader_matches_reference_outcomes(tmp_path, name):
+    """The native reader (sgns_vectors_header / sgns_vectors_sniff / sgns_parse_vectors with
+    the Python per-row fallback) against the reference's own load_model and detect_format
+    on a torture set (tests/golden/make_golden.py gen_read): Python number syntax
+    (underscores, inf/nan, fullwidth and Arabic-Indic digits), universal newlines, tabs
+    inside fields, blank lines, doubled spaces, duplicate tokens, truncation, malformed
+    headers, binary files without newlines or with newline-prefixed tokens, invalid UTF-8."""
+    g, _ = _read_cases()
+    path = str(tmp_path / name)
+    with open(path, "wb") as fh:
+        fh.write(g[f"{name}__bytes"].tobytes())
+    flag = int(g[f"{name}__binary"])
+    binary = None if flag < 0 else bool(flag)
+    if f"{name}__sniff" in g:
+        assert detect_format(path) is bool(int(g[f"{name}__sniff"]))
+    else:
+        with pytest.raises(ModelFormatError):
+            detect_format(path)
+    if f"{name}__error" in g:
+        kind, msg = str(g[f"{name}__error"]).split(": ", 1)
+        with pytest.raises(Exception) as ei:
+            load_model(path, binary)
+        assert type(ei.value).__name__ == kind
+        if kind != "UnicodeDecodeError":  # byte positions are relative to what was decoded
+            assert str(ei.value).replace(path, "<path>") == msg
+        return
+    model, voc = load_model(path, binary)
+    assert voc.tokens == str(g[f"{name}__tokens"]).split("\x00")
+    assert np.array_equal(model.input_vectors.view(np.uint32), g[f"{name}__vecs"])
+    assert voc.index == {t: i for i, t in enumerate(voc.tokens)}
