@@ -197,6 +197,19 @@ int sgns_vectors_sniff(const char *path, int64_t header_bytes, int32_t dim, int3
 int sgns_parse_vectors(const char *path, int32_t binary, int64_t vocab, int32_t dim, float *vectors,
                        int64_t *tok_start, int64_t *tok_end, int64_t *row, int64_t *offset);
 
+/* Analogy evaluation on the device (replaces the numpy part of eval_analogy,
+ * sgns/evaluate.py:164-212; sgns_eval.cu).
+ *   sgns_unit_rows:    out = rows / ||rows|| per row, float32, bit-identical to numpy's
+ *                      vectors / np.linalg.norm(vectors, axis=1) (zero norm -> 1).
+ *   sgns_analogy_top1: for each question (a, b, c) (q3: nq x 3 row ids < n), best[q] =
+ *                      argmax over rows w < n, w not in {a, b, c}, of ((u_b - u_a) + u_c) . u_w
+ *                      (first index on ties); workspace: nq * dim * 4 + 4 + nq * 8 bytes of
+ *                      device memory, 8-byte aligned.  All pointers are device pointers. */
+int sgns_unit_rows(const float *rows, int64_t ld, int64_t n, int32_t dim, float *out, int64_t ld_out,
+                   void *stream);
+int sgns_analogy_top1(const float *unit, int64_t ld, int64_t n, int32_t dim, const int32_t *q3, int64_t nq,
+                      int32_t *best, void *workspace, void *stream);
+
 const char *sgns_error_string(int32_t code);
 int sgns_abi_version(void);
 /* sizeof(sgns_worker), sizeof(sgns_drive_params): lets bindings check their layout. */

@@ -103,6 +103,10 @@ def lib() -> C.CDLL:
     L.sgns_vectors_sniff.argtypes = [C.c_char_p, I64, I32, C.POINTER(I32)]
     L.sgns_parse_vectors.restype = C.c_int
     L.sgns_parse_vectors.argtypes = [C.c_char_p, I32, I64, I32, P, P, P, C.POINTER(I64), C.POINTER(I64)]
+    L.sgns_unit_rows.restype = C.c_int
+    L.sgns_unit_rows.argtypes = [P, I64, I64, I32, P, I64, P]
+    L.sgns_analogy_top1.restype = C.c_int
+    L.sgns_analogy_top1.argtypes = [P, I64, I64, I32, P, I64, P, P, P]
     L.sgns_struct_sizes.restype = C.c_int
     L.sgns_struct_sizes.argtypes = [C.POINTER(I32), C.POINTER(I32)]
     if L.sgns_abi_version() != 2:
@@ -120,7 +124,8 @@ EXPORTED = ("sgns_update_windows", "sgns_drive", "sgns_init_model", "sgns_expand
             "sgns_build_alias", "sgns_resident_workers", "sgns_error_string", "sgns_abi_version",
             "sgns_struct_sizes", "sgns_vocab_build", "sgns_vocab_from_tokens", "sgns_vocab_export",
             "sgns_vocab_free", "sgns_encode", "sgns_encoded_export", "sgns_encoded_free",
-            "sgns_write_vectors", "sgns_vectors_header", "sgns_vectors_sniff", "sgns_parse_vectors")
+            "sgns_write_vectors", "sgns_vectors_header", "sgns_vectors_sniff", "sgns_parse_vectors",
+            "sgns_unit_rows", "sgns_analogy_top1")
 
 
 class SgnsError(RuntimeError):

@@ -64,3 +64,48 @@ def test_analogy_matches_reference(tmp_path):
     from paper_1604_04661_b200.model import DeviceModel
     acc3, _, _ = eval_analogy(DeviceModel.from_host(model), voc, ana)
     assert acc3 == acc
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim", [1, 7, 8, 100, 128, 129, 300, 517])
+def test_unit_rows_bit_identical_to_numpy(dim):
+    """sgns_unit_rows == vectors / np.linalg.norm(vectors, axis=1) (zero norm -> 1) bit for
+    bit: numpy's pairwise float32 summation order, across its 8 / 128 / halving regimes."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    from paper_1604_04661_b200.evaluate import unit_rows
+    rng = np.random.default_rng(dim)
+    v = (rng.normal(size=(333, dim)) * 10.0 ** rng.integers(-3, 3, size=(333, 1))).astype(np.float32)
+    v[5] = 0.0
+    norms = np.linalg.norm(v, axis=1, keepdims=True)
+    norms[norms == 0.0] = 1.0
+    want = v / norms
+    got = unit_rows(torch.from_numpy(v).cuda(), dim, len(v)).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,dim,nq", [(5, 3, 4), (1000, 300, 257), (40_000, 100, 1500)])
+def test_analogy_top1_vs_brute_force(n, dim, nq):
+    """The fused score/argmax kernel against a float64 brute force: the same row except where
+    the float64 top two lie within float32 rounding of each other (a legal tie flip)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    from paper_1604_04661_b200.evaluate import analogy_top1
+    rng = np.random.default_rng(n + dim)
+    u = rng.normal(size=(n, dim)).astype(np.float32)
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    q = np.stack([rng.choice(n, size=3, replace=False) for _ in range(nq)]).astype(np.int32)
+    got = analogy_top1(torch.from_numpy(u).cuda(), q)
+    t = (u[q[:, 1]] - u[q[:, 0]] + u[q[:, 2]]).astype(np.float64)
+    s = t @ u.astype(np.float64).T
+    s[np.arange(nq)[:, None], q] = -np.inf
+    want = s.argmax(axis=1)
+    top = np.sort(s, axis=1)[:, -2:]
+    close = (top[:, 1] - top[:, 0]) < 1e-5 * np.abs(top[:, 1]).clip(1.0)
+    bad = (got != want) & ~close
+    assert not bad.any(), np.flatnonzero(bad)[:5]
+    assert (got == want).mean() > 0.99
+    assert not (got[:, None] == q).any()  # never a question word
