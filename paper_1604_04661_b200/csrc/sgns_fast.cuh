@@ -390,7 +390,6 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
 
       // scores, errors, dA -- inputs in pairs so one transposed butterfly (16 values,
       // 5 serial shuffle stages) reduces both inputs' scores
-      const float2 alpha2 = make_float2(alpha, alpha);
       for (int i = 0; i < m; i += 2) {
         const bool two = i + 1 < m;
         float pp[2 * NV];
@@ -433,14 +432,19 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
             cnt_s[4] += nc;
           }
         }
+        // dA_i = sum_k (alpha err_ik) C_k (alpha folded into e, as batch_core_blas,
+        // kernel_batched.py:92-144): the pair's error rows are broadcast from e_s
+        __syncwarp();
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (h == 1 && !two) break;
+          const float4 e03 = *reinterpret_cast<const float4 *>(e_s + (i + h) * 8);
+          const float4 e47 = *reinterpret_cast<const float4 *>(e_s + (i + h) * 8 + 4);
+          const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
           float2 d[NS];
 #pragma unroll
           for (int k = 0; k < K1R; ++k) {
-            const float ek = __shfl_sync(0xffffffffu, er, 2 * (h * NV + k));
-            const float2 ek2 = make_float2(ek, ek);
+            const float2 ek2 = make_float2(kk_ok(k) ? ev[k] : 0.f, kk_ok(k) ? ev[k] : 0.f);
 #pragma unroll
             for (int j = 0; j < NS; ++j)
               d[j] = k == 0 ? __fmul2_rn(ek2, c_reg[0][j]) : __ffma2_rn(ek2, c_reg[k][j], d[j]);
@@ -448,7 +452,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
           float *dst = in_dst_l + off_s[i + h];
 #pragma unroll
           for (int j = 0; j < NS; ++j)
-            if (slot_ok(j)) atomicAdd(reinterpret_cast<float2 *>(dst + 64 * j), __fmul2_rn(d[j], alpha2));
+            if (slot_ok(j)) atomicAdd(reinterpret_cast<float2 *>(dst + 64 * j), d[j]);
         }
       }
       // C registers are free: finish u+1's negatives and start loading its output rows
