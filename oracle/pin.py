@@ -104,11 +104,11 @@ def replay_sentences(run, dm, n_sentences: int, cap: int, k1: int, sig_table) ->
                 out["shared_next"] += 1
             prev_out = outs
             out["windows"] += 1
-        if len(new):
-            out["loss_worst"] = max(out["loss_worst"], abs(gpu_loss - exp_loss) / (1e-5 * abs(exp_loss) + 1e-9))
-        if edge:
+        if edge:  # a legal bin flip changes the windows after it: model and loss both skipped
             out["flagged"] += 1
             continue
+        if len(new):
+            out["loss_worst"] = max(out["loss_worst"], abs(gpu_loss - exp_loss) / (1e-5 * abs(exp_loss) + 1e-9))
         after = dm.to_host()
         out["worst"] = max(out["worst"], budget_used(after.input_vectors, mi),
                            budget_used(after.output_vectors, mo))

@@ -71,8 +71,8 @@ __host__ __device__ inline FastSlab fast_slab(int64_t ld, int mcap, int k1r, int
   s.kept = s.roff + round16_(int64_t(2) * idsn * 4);
   s.koff = s.kept + round16_(int64_t(kept_cap) * 4);
   s.bw = s.koff + round16_(int64_t(kept_cap) * 4);
-  s.cnt = s.bw + round16_(int64_t(kept_cap) * 4);  // 6 x 8-byte counters, lane 0 only
-  s.total = s.cnt + 48;
+  s.cnt = s.bw + round16_(int64_t(kept_cap) * 4);  // 5 counters, the loss, a pair's claim
+  s.total = s.cnt + 64;
   return s;
 }
 
@@ -183,19 +183,38 @@ __device__ __forceinline__ void select_negatives(const FastArgs &p, NegCand cnd,
 template <int NS, int K1R> struct FastRegs {
   static constexpr int v = (K1R > 6 && NS >= 5) ? SGNS_FAST_MAXNREG_WIDE : SGNS_FAST_MAXNREG;
 };
-template <int NS, int NCH, int K1R, bool EXACT_K, bool FULL>
+// Warp pairs: with PAIR, a worker is TWO warps of the block (warps 2t, 2t+1) for
+// K + 1 = 9..16 output rows: warp r holds output rows [r K1R, r K1R + kown) of every window
+// in registers (K1R = ceil((K + 1) / 2)), so no warp needs more than 8 output rows of
+// registers.  Both warps walk the same control stream (subsampling, windows, negatives:
+// deterministic Philox, recomputed by each), stage their own copy of the window's input
+// rows, and scatter their own dC rows and their partial dA_i = sum over their outputs.
+// Two pair barriers per window keep the worker's order exact: after both copies of the
+// window's rows are staged (no scatter of the window starts before both warps read its
+// rows) and after both warps' scatters (the next window's gathers see both).  A prefetched
+// output row of the next window that the OTHER warp updates in this window is reloaded
+// after the second barrier; rows shared within a warp are patched as in the single-warp
+// form.  Leader warp (r = 0) alone claims sentences, counts, traces and marks rows.
+__device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+
+template <int NS, int NCH, int K1R, bool EXACT_K, bool FULL, bool PAIR = false>
 __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p) {
   constexpr int NV = 8;
+  constexpr int K1T = PAIR ? 2 * K1R : K1R;  // output ids held per window
   extern __shared__ __align__(16) unsigned char smem[];
   float *sig_s = reinterpret_cast<float *>(smem);
   for (int i = threadIdx.x; i < kSigBins; i += blockDim.x) sig_s[i] = p.sig[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wid = blockIdx.x * p.wpb + warp;
+  const int wid = PAIR ? (blockIdx.x * p.wpb + warp) >> 1 : blockIdx.x * p.wpb + warp;
   if (wid >= p.n_workers) return;
-  const int k1 = EXACT_K ? K1R : p.k_neg + 1;
+  const bool lead = !PAIR || (warp & 1) == 0;
+  const int bar_id = 1 + (warp >> 1);  // PAIR: named barrier of this warp pair
+  const int k1 = PAIR ? p.k_neg + 1 : (EXACT_K ? K1R : p.k_neg + 1);  // outputs per window
+  const int kbase = PAIR && !lead ? K1R : 0;                          // this warp's first output
+  const int kown = PAIR ? (lead ? K1R : k1 - K1R) : k1;                // and how many
   const int mcap = min(p.cap, 2 * p.window);
-  const FastSlab L = fast_slab(p.mv.ld, mcap, K1R, p.kept_cap);
+  const FastSlab L = fast_slab(p.mv.ld, mcap, K1T, p.kept_cap);
   unsigned char *base = smem + round16_(kSigBins * 4) + (int64_t)warp * L.total;
   float *rows_s = reinterpret_cast<float *>(base + L.rows);
   float *e_s = reinterpret_cast<float *>(base + L.e);
@@ -216,8 +235,14 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
   // lane 0: move the current epoch's loss into the per-epoch and per-launch totals
   auto flush_epoch_loss = [&](int e) {
     if (lane == 0) {
-      p.loss_by_epoch[(int64_t)wid * p.epochs + e] += *loss_s;
-      p.cells_by_epoch[(int64_t)wid * p.epochs + e] += cnt_s[4];
+      if (PAIR) {  // both warps of the pair sum into the worker's slots
+        atomicAdd(p.loss_by_epoch + (int64_t)wid * p.epochs + e, *loss_s);
+        atomicAdd(reinterpret_cast<unsigned long long *>(p.cells_by_epoch + (int64_t)wid * p.epochs + e),
+                  (unsigned long long)cnt_s[4]);
+      } else {
+        p.loss_by_epoch[(int64_t)wid * p.epochs + e] += *loss_s;
+        p.cells_by_epoch[(int64_t)wid * p.epochs + e] += cnt_s[4];
+      }
       if (p.totals != nullptr) {
         atomicAdd(p.totals + 4, (unsigned long long)cnt_s[4]);
         atomicAdd(p.loss_total, *loss_s);
@@ -226,7 +251,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
       cnt_s[4] = 0;
     }
   };
-  const int idsn = mcap + K1R;
+  const int idsn = mcap + K1T;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int ld = (int)p.mv.ld;  // shared-memory indexing in 32 bits
   const int nvec = p.mv.nvec, nslot = 2 * nvec;
@@ -238,14 +263,22 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
   const float *const in_src_l = p.mv.in_src + 4 * lane;
   auto slot_ok = [&](int j) { return FULL || j < NS - 1 || lane + 32 * j < nslot; };
   auto chunk_ok = [&](int j) { return j < NCH - 1 || lane + 32 * j < nvec; };
-  auto kk_ok = [&](int k) { return EXACT_K || k < k1; };
+  auto kk_ok = [&](int k) { return EXACT_K || k < kown; };
   const int rec_len = 4 + p.cap + k1;
 
   int loss_epoch = -1;
 
   for (;;) {
     unsigned long long c = 0;
-    if (lane == 0) c = atomicAdd(p.claim, 1ULL);
+    if (lane == 0 && lead) c = atomicAdd(p.claim, 1ULL);
+    if (PAIR) {  // the leader's claim, through its slab's spare counter slot
+      volatile unsigned long long *xch = reinterpret_cast<unsigned long long *>(
+          smem + round16_(kSigBins * 4) + (int64_t)(warp & ~1) * L.total + L.cnt) + 6;
+      if (lane == 0 && lead) *xch = c;
+      pair_bar(bar_id);
+      c = *xch;
+      pair_bar(bar_id);  // read before the leader's next claim overwrites it
+    }
     c = __shfl_sync(0xffffffffu, c, 0);
     if ((int64_t)c >= p.claim_end) break;
     const int epoch = (int)((int64_t)c / p.n_sent);
@@ -257,7 +290,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
       continue;
     }
     const uint32_t ep = p.epoch_base + (uint32_t)epoch;
-    if (lane == 0) cnt_s[1] += n;
+    if (lane == 0 && lead) cnt_s[1] += n;
     // alpha from the sentence's words-read position (update_alpha, trainer.py:122-132)
     // (the shard's bounds are re-read per sentence -- two cached loads -- rather than
     // held in four registers across the hot loop)
@@ -302,7 +335,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
       bw_s[q] = b;
     }
     __syncwarp();
-    if (lane == 0) cnt_s[0] += nk;
+    if (lane == 0 && lead) cnt_s[0] += nk;
 
     Unit u;
     if (!first_unit(bw_s, nk, p.cap, u)) continue;
@@ -329,7 +362,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
       const uint32_t *off_s = roff_b;
 #pragma unroll
       for (int k = 0; k < K1R; ++k) {
-        const float *src = out_src_l + off_s[u.mc + (kk_ok(k) ? k : 0)];
+        const float *src = out_src_l + off_s[u.mc + kbase + (kk_ok(k) ? k : 0)];
 #pragma unroll
         for (int j = 0; j < NS; ++j)
           c_reg[k][j] = (kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 64 * j) : f2zero();
@@ -350,7 +383,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
         for (int j = 0; j < NCH; ++j)
           if (chunk_ok(j)) cp_async16(dst + 128 * j, src + 128 * j);
       }
-      if (p.dirty != nullptr) {  // touched rows (data-parallel touched-row averaging)
+      if (p.dirty != nullptr && lead) {  // touched rows (data-parallel touched-row averaging)
         for (int r = lane; r < m + k1; r += 32) p.dirty[(r < m ? 0u : p.vocab) + (uint32_t)ids_s[r]] = 1;
       }
       // next unit + its negative candidates (alias loads in flight during u's math)
@@ -362,11 +395,11 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
         tok_n = (uint64_t)(p.token_base + lo_t + koff_s[nx.pos]);
         if (lane < min(32, p.k_neg + 2)) cand_n = neg_candidate(p, tok_n, ep, nx.ch, lane);
       }
-      if (lane == 0) {
+      if (lane == 0 && lead) {
         cnt_s[2] += 1;
         cnt_s[3] += m;
       }
-      if (p.trace_cap > 0) {
+      if (p.trace_cap > 0 && lead) {
         unsigned long long idx = 0;
         if (lane == 0) idx = atomicAdd(p.trace_count, 1ULL);
         idx = __shfl_sync(0xffffffffu, idx, 0);
@@ -387,6 +420,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
       }
       cp_async_wait_all();
       __syncwarp();
+      if (PAIR) pair_bar(bar_id);  // both copies staged: no scatter of u before both read its rows
 
       // scores, errors, dA -- inputs in pairs so one transposed butterfly (16 values,
       // 5 serial shuffle stages) reduces both inputs' scores
@@ -418,12 +452,12 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
         const int v = reduced_index<2 * NV>(lane);
         const int hk = v >> 3, kk = v & 7;
         float er = 0.f, es = 0.f;
-        const bool live = kk < k1 && (hk == 0 || two);
-        cell_error_f32(sc, kk, alpha, sig_s, er, es);
+        const bool live = kk < kown && (hk == 0 || two);
+        cell_error_f32(sc, kk + kbase, alpha, sig_s, er, es);
         if (live) e_s[(i + hk) * 8 + kk] = es;  // both lanes of the pair hold the same value
         if (want) {  // sampled sentence: warp-reduce this pair's softplus terms
           const bool mine = live && (lane & 1) == 0;
-          double sp = mine ? softplus(kk == 0 ? -(double)sc : (double)sc) : 0.0;
+          double sp = mine ? softplus(kk + kbase == 0 ? -(double)sc : (double)sc) : 0.0;
 #pragma unroll
           for (int o = 16; o >= 1; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
           const int nc = __popc(__ballot_sync(0xffffffffu, mine));
@@ -457,7 +491,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
       }
       // C registers are free: finish u+1's negatives and start loading its output rows
       // bit (8 k + k') of lo_bits (k < 4) / hi_bits (k >= 4): out(u)[k] == out(u+1)[k']
-      unsigned lo_bits = 0, hi_bits = 0;
+      unsigned lo_bits = 0, hi_bits = 0, cross_bits = 0;
       if (have) {
         for (int r = lane; r < nx.mc; r += 32) {
           const int q = nx.start + r;
@@ -469,14 +503,22 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
         __syncwarp();
         for (int r = lane; r < nx.mc + k1; r += 32) off_n[r] = (uint32_t)ids_n[r] * (uint32_t)ld;
         const int kq = lane & 7, ka = lane >> 3, kb = 4 + (lane >> 3);
-        const bool h1 = ka < k1 && kq < k1 && ids_s[m + ka] == ids_n[nx.mc + kq];
-        const bool h2 = kb < k1 && kq < k1 && ids_s[m + kb] == ids_n[nx.mc + kq];
+        const bool h1 = ka < kown && kq < kown && ids_s[m + kbase + ka] == ids_n[nx.mc + kbase + kq];
+        const bool h2 = kb < kown && kq < kown && ids_s[m + kbase + kb] == ids_n[nx.mc + kbase + kq];
         lo_bits = __ballot_sync(0xffffffffu, h1);
         hi_bits = __ballot_sync(0xffffffffu, h2);
+        if (PAIR) {
+          // bit kq: this warp's output kq of u+1 is a row the OTHER warp updates in u
+          const int obase = lead ? K1R : 0, oown = k1 - kown;
+          bool x = false;
+          if (lane < kown)
+            for (int o = 0; o < oown; ++o) x |= ids_n[nx.mc + kbase + lane] == ids_s[m + obase + o];
+          cross_bits = __ballot_sync(0xffffffffu, x);
+        }
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < K1R; ++k) {
-          const float *src = out_src_l + off_n[nx.mc + (kk_ok(k) ? k : 0)];
+          const float *src = out_src_l + off_n[nx.mc + kbase + (kk_ok(k) ? k : 0)];
 #pragma unroll
           for (int j = 0; j < NS; ++j)
             c_reg[k][j] = (kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 64 * j) : f2zero();
@@ -486,7 +528,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
       // dC_k = sum_i (alpha err_ik) A_i, column-outer; patch u+1's prefetched copies.
       uint32_t orow[K1R];  // 32-bit row offsets: one IMAD.WIDE per scatter, 6 registers
 #pragma unroll
-      for (int k = 0; k < K1R; ++k) orow[k] = off_s[m + (kk_ok(k) ? k : 0)];
+      for (int k = 0; k < K1R; ++k) orow[k] = off_s[m + kbase + (kk_ok(k) ? k : 0)];
 #pragma unroll
       for (int j = 0; j < NS; ++j) {
         if (!slot_ok(j)) continue;
@@ -521,6 +563,19 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
         }
       }
       __syncwarp();
+      if (PAIR) {
+        pair_bar(bar_id);  // both warps' scatters of u precede the gathers of u+1
+        if (cross_bits) {  // reload rows the other warp updated in u (its dC is now visible)
+#pragma unroll
+          for (int k = 0; k < K1R; ++k) {
+            if (!(cross_bits & (1u << k))) continue;
+            const float *src = out_src_l + off_n[nx.mc + kbase + k];
+#pragma unroll
+            for (int j = 0; j < NS; ++j)
+              if (slot_ok(j)) c_reg[k][j] = ld_cg_f2(src + 64 * j);
+          }
+        }
+      }
       if (have) {
         u = nx;
         cur ^= 1;
@@ -531,6 +586,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
   if (loss_epoch >= 0) flush_epoch_loss(loss_epoch);
   __syncwarp();
   const long long trained = cnt_s[0], read = cnt_s[1], chunks = cnt_s[2], inputs = cnt_s[3];
+  if (!lead) return;
   if (lane == 0 && p.totals != nullptr) {
     atomicAdd(p.totals + 0, (unsigned long long)trained);
     atomicAdd(p.totals + 1, (unsigned long long)read);

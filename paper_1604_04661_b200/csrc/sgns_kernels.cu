@@ -18,9 +18,9 @@
 #include "sgns_device.cuh"
 #include "sgns_fast.cuh"
 
-// The library is built from this one file as four translation units compiled in parallel
+// The library is built from this one file as five translation units compiled in parallel
 // (SGNS_PART 0: C ABI + init/slot kernels, 1: update_windows, 2: static driver, 3: fast
-// driver; see __graft_entry__.build_lib).  Without SGNS_PART it is a single unit.
+// driver, 4: fast driver in warp pairs; see __graft_entry__.build_lib).  Without SGNS_PART it is a single unit.
 // SGNS_ONLY_NS=n (experiment builds, tools/build_variant.py) instantiates the dynamic
 // driver for one row width only.
 #ifdef SGNS_PART
@@ -950,6 +950,8 @@ static int fast_ns(FastArgs a, int wpb, cudaStream_t st, int *res) {
               : launch_fast_t<NS, 6, false, false>(a, wpb, st, res);
 }
 
+int pair_dispatch(const FastArgs &a, int64_t ld, int wpb, cudaStream_t st, int *resident);
+
 int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
   FastArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -994,6 +996,7 @@ int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
   a.loss_total = p->d_loss_total;
   a.dirty = p->d_dirty;
   const int wpb = p->warps_per_block;
+  if (p->k_neg + 1 > 8) return pair_dispatch(a, p->ld, wpb, st, resident);  // warp pairs
   switch (ns_for(p->ld)) {
 #if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 1
     case 1: return fast_ns<1>(a, wpb, st, resident);
@@ -1025,11 +1028,91 @@ int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
 
 #endif  // SGNS_HAS(3)
 
+#if SGNS_HAS(4)
+// ------------------------------------------------- fast path, warp pairs ----
+// K + 1 = 9..16: a worker is a pair of warps, each holding ceil((K + 1) / 2) output rows
+// (drive_fast_kernel<..., PAIR>); n_workers counts pairs.
+template <int NS, int K1R, bool FULL>
+static int launch_pair_t(FastArgs a, int wpb_req, cudaStream_t st, int *resident) {
+  constexpr int NCH = (NS + 1) / 2;
+  auto kern = drive_fast_kernel<NS, NCH, K1R, false, FULL, true>;
+  const FastSlab L = fast_slab(a.mv.ld, std::min(a.cap, 2 * a.window), 2 * K1R, a.kept_cap);
+  int best = -1, wpb = 2, bps = 1;
+  for (int w : {2, 4, 8, 16}) {  // warps per block: whole pairs
+    const int64_t bytes = table_bytes(4) + (int64_t)w * L.total;
+    if (bytes > 227 * 1024 || prepare(kern, bytes) != 0) break;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, w * 32, (size_t)bytes) != cudaSuccess) break;
+    if (nb * w > best) {
+      best = nb * w;
+      wpb = w;
+      bps = nb;
+    }
+  }
+  if (best <= 0) return SGNS_E_SMEM;
+  if (resident) {
+    *resident = wpb * bps * num_sms() / 2;
+    return 0;
+  }
+  if (wpb_req > 0) wpb = wpb_req & ~1;
+  if (wpb < 2) return SGNS_E_ARG;
+  a.wpb = wpb;
+  const int64_t bytes = table_bytes(4) + (int64_t)wpb * L.total;
+  int rc;
+  if ((rc = prepare(kern, bytes))) return rc;
+  const int grid = (int)((2 * (int64_t)a.n_workers + wpb - 1) / wpb);
+  kern<<<grid, wpb * 32, bytes, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+template <int NS>
+static int pair_ns(const FastArgs &a, int64_t ld, int wpb, cudaStream_t st, int *res) {
+  const bool full = ld == 64 * NS;
+  switch ((a.k_neg + 2) / 2) {  // ceil((K + 1) / 2)
+    case 5: return full ? launch_pair_t<NS, 5, true>(a, wpb, st, res) : launch_pair_t<NS, 5, false>(a, wpb, st, res);
+    case 6: return full ? launch_pair_t<NS, 6, true>(a, wpb, st, res) : launch_pair_t<NS, 6, false>(a, wpb, st, res);
+    case 7: return full ? launch_pair_t<NS, 7, true>(a, wpb, st, res) : launch_pair_t<NS, 7, false>(a, wpb, st, res);
+    case 8: return full ? launch_pair_t<NS, 8, true>(a, wpb, st, res) : launch_pair_t<NS, 8, false>(a, wpb, st, res);
+  }
+  return SGNS_E_SHAPE;
+}
+
+int pair_dispatch(const FastArgs &a, int64_t ld, int wpb, cudaStream_t st, int *resident) {
+  switch (ns_for(ld)) {
+#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 1
+    case 1: return pair_ns<1>(a, ld, wpb, st, resident);
+#endif
+#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 2
+    case 2: return pair_ns<2>(a, ld, wpb, st, resident);
+#endif
+#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 3
+    case 3: return pair_ns<3>(a, ld, wpb, st, resident);
+#endif
+#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 4
+    case 4: return pair_ns<4>(a, ld, wpb, st, resident);
+#endif
+#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 5
+    case 5: return pair_ns<5>(a, ld, wpb, st, resident);
+#endif
+#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 6
+    case 6: return pair_ns<6>(a, ld, wpb, st, resident);
+#endif
+#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 7
+    case 7: return pair_ns<7>(a, ld, wpb, st, resident);
+#endif
+#if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 8
+    case 8: return pair_ns<8>(a, ld, wpb, st, resident);
+#endif
+  }
+  return SGNS_E_SHAPE;
+}
+#endif  // SGNS_HAS(4)
+
 
 #if SGNS_HAS(0)
 static bool fast_eligible(const sgns_drive_params *p) {
   const int64_t ld = p->ld;
-  return p->dtype == SGNS_F32 && p->rng_mode == SGNS_RNG_PHILOX && p->k_neg + 1 <= 8 &&
+  return p->dtype == SGNS_F32 && p->rng_mode == SGNS_RNG_PHILOX && p->k_neg + 1 <= 16 &&
          ns_for(ld) >= 1 && ns_for(ld) <= 8 && offsets32_ok(p->vocab, ld) &&
          p->sigmoid_mode == SGNS_SIGMOID_TABLE;
 }

@@ -122,11 +122,11 @@ class TrainingConfig:
             raise ConfigError("rng='philox' supports at most 256 chunks per position "
                               "(ceil(2 * window / batch_cap) <= 256)")
         if self.schedule == "dynamic" and not self.dynamic_eligible(0):
-            raise ConfigError("schedule='dynamic' needs rng='philox', float32, negatives <= 7, dim <= 512")
+            raise ConfigError("schedule='dynamic' needs rng='philox', float32, negatives <= 15, dim <= 512")
 
     def dynamic_eligible(self, vocab_size: int) -> bool:
         ld = -(-self.dim // 4) * 4
-        return (self.rng == "philox" and not self.float64 and self.negatives + 1 <= 8
+        return (self.rng == "philox" and not self.float64 and self.negatives + 1 <= 16
                 and -(-(ld // 2) // 32) <= 8 and vocab_size * ld < 2**32)
 
     def use_dynamic(self, vocab_size: int) -> bool:
@@ -540,7 +540,7 @@ class StreamingTrainer:
         config.validate()
         if not config.use_dynamic(model.vocab_size):
             raise ConfigError("streaming training needs the dynamic schedule "
-                              "(rng='philox', float32, negatives <= 7, dim <= 512)")
+                              "(rng='philox', float32, negatives <= 15, dim <= 512)")
         self.torch = torch
         self.model, self.config = model, config
         dev = model.m_in.device

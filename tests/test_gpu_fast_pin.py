@@ -59,6 +59,11 @@ def _fast_run(ids, off, counts, dm, *, k, cap, window=5, seed=9, alpha0=0.025):
 # (d = 64, 320, 512) and partial last slots (d = 4, 100, 300); cap 4 splits positions.
 CASES = [(d, k, 16) for d in (100, 300, 512) for k in (3, 4, 5, 6, 7)]
 CASES += [(4, 5, 16), (4, 7, 16), (64, 2, 16), (320, 5, 16), (300, 5, 4), (100, 7, 4), (512, 3, 4)]
+# K + 1 = 9..16: warp pairs (each warp ceil((K + 1) / 2) output rows; odd K + 1 leaves the
+# second warp one row short).  With 12 ids and up to 15 negatives, rows of the next window
+# are shared with BOTH warps' rows all the time (the cross-warp reload path).
+CASES += [(300, k, 16) for k in (8, 9, 10, 12, 14, 15)] + [(100, 10, 16), (512, 15, 16), (4, 11, 16),
+                                                          (320, 15, 16), (300, 15, 4), (64, 9, 4)]
 
 
 def _pin_case(D, k, cap, window=5, V=12, n_sent=60, lo=4, hi=12, seed_extra=0):
