@@ -1,5 +1,6 @@
 // sgns_fast.cuh -- production driver: Philox draws, dynamic sentence claiming and a
-// two-stage software pipeline across windows (float32, K + 1 <= 8, d <= 512).
+// two-stage software pipeline across windows (float32, d <= 512, K + 1 <= 16: one warp
+// per worker up to K + 1 = 8, a pair of warps above).
 //
 // Differences from drive_kernel (the reference-stream driver), all invisible to the
 // update math:
