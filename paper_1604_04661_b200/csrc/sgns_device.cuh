@@ -409,7 +409,6 @@ __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const Mo
   const int lane = sh.lane;
   cp_async_wait_all();
   __syncwarp();  // staged rows were copied in 16-byte lanes, read in 8-byte lanes
-  const float2 alpha2 = make_float2(alpha, alpha);
   float *in_dst_l = mv.in_dst + 2 * lane;
   // inputs in pairs: one transposed butterfly over 16 values reduces both inputs' scores
   for (int i = 0; i < m; i += 2) {
@@ -450,13 +449,19 @@ __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const Mo
         }
       }
     }
+    // dA_i = sum_k (alpha err_ik) C_k, alpha folded into e as batch_core_blas does
+    // (kernel_batched.py:92-144): the pair's error rows are broadcast from e_s
+    __syncwarp();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (h == 1 && !two) break;
+      const float4 e03 = *reinterpret_cast<const float4 *>(e_s + (i + h) * 8);
+      const float4 e47 = *reinterpret_cast<const float4 *>(e_s + (i + h) * 8 + 4);
+      const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
       float2 d[NS];
 #pragma unroll
       for (int k = 0; k < K1R; ++k) {
-        const float ek = __shfl_sync(0xffffffffu, er, 2 * (h * NV + k));
+        const float ek = (EXACT_K || k < k1) ? ev[k] : 0.f;
         const float2 ek2 = make_float2(ek, ek);
 #pragma unroll
         for (int j = 0; j < NS; ++j) d[j] = k == 0 ? __fmul2_rn(ek2, c[0][j]) : __ffma2_rn(ek2, c[k][j], d[j]);
@@ -469,17 +474,17 @@ __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const Mo
           for (int j = 0; j < NS; ++j)
             if (sh.slot_ok(j)) {
               float2 *q = reinterpret_cast<float2 *>(hs + 64 * j);
-              *q = __fadd2_rn(*q, __fmul2_rn(d[j], alpha2));
+              *q = __fadd2_rn(*q, d[j]);
             }
         } else {
 #pragma unroll
-          for (int j = 0; j < NS; ++j) hot.reg[j] = __fadd2_rn(hot.reg[j], __fmul2_rn(d[j], alpha2));
+          for (int j = 0; j < NS; ++j) hot.reg[j] = __fadd2_rn(hot.reg[j], d[j]);
         }
       } else {
         float *dst = in_dst_l + ro;
 #pragma unroll
         for (int j = 0; j < NS; ++j)
-          if (sh.slot_ok(j)) atomicAdd(reinterpret_cast<float2 *>(dst + 64 * j), __fmul2_rn(d[j], alpha2));
+          if (sh.slot_ok(j)) atomicAdd(reinterpret_cast<float2 *>(dst + 64 * j), d[j]);
       }
     }
   }
