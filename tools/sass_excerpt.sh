@@ -2,12 +2,12 @@
 # SASS evidence for the production kernel: instruction histogram, the packed-FP32 / async-copy
 # / vector-reduction instruction forms, and the dC inner loop.
 #   bash tools/sass_excerpt.sh > profiles/round2_drive_fast_kernel_sass.txt
-FUN=_ZN4sgns17drive_fast_kernelILi5ELi3ELi6ELb1ELb0EEEvNS_8FastArgsE
+FUN=_ZN4sgns17drive_fast_kernelILi5ELi3ELi6ELb1ELb0ELb0EEEvNS_8FastArgsE
 LIB=$(dirname "$0")/../paper_1604_04661_b200/libsgns_b200.so
 T=$(mktemp)
 cuobjdump -sass -fun $FUN "$LIB" 2>/dev/null > $T
 echo "# cuobjdump -sass -fun $FUN paper_1604_04661_b200/libsgns_b200.so"
-echo "# (drive_fast_kernel<NS=5,NCH=3,K1R=6,EXACT_K,!FULL>: the bench's d=300, K=5 instantiation)"
+echo "# (drive_fast_kernel<NS=5,NCH=3,K1R=6,EXACT_K,!FULL,!PAIR>: the bench's d=300, K=5 instantiation)"
 echo "## opcode histogram (static instruction count)"
 grep -oE "^\s+/\*[0-9a-f]+\*/\s+(@!?U?P[0-9T] )?[A-Z0-9_]+" $T | awk '{print $NF}' | sort | uniq -c | sort -rn | head -30
 echo "## packed FP32, async copies, vector reductions (full forms)"
