@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -134,8 +135,17 @@ template <typename T> struct UpdateArgs {
   int hot_in, hot_out;  // shared-memory hot-row sink rows (HOT launches; hot_in 0: register sink)
 };
 
+// Register budget of update_windows_kernel: 128 (16 warps per SM) for the register-row
+// float32 bodies, except 7-8 output rows of >= 5 slots (d > 256) -- F2G's first group always
+// has 8 -- which get up to 168 (12-13 warps) instead of spilling, as the fast driver does;
+// the all-staged generic body 255.
+template <int MODE, int NS, int K1R> struct UpdRegs {
+  static constexpr int v = MODE == MODE_SMEM ? 255
+                           : ((MODE == MODE_F2 && K1R >= 7) || MODE == MODE_F2G) && NS >= 5
+                               ? SGNS_FAST_MAXNREG_WIDE : 128;
+};
 template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT>
-__global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) update_windows_kernel(UpdateArgs<T> p) {
+__global__ void __maxnreg__((UpdRegs<MODE, NS, K1R>::v)) update_windows_kernel(UpdateArgs<T> p) {
   extern __shared__ __align__(16) unsigned char smem[];
   T *sig_s = reinterpret_cast<T *>(smem);
   load_table(sig_s, p.sig);
@@ -264,7 +274,7 @@ struct SmBatch {
 };
 
 template <typename T, int MODE, int NS, int NCH, int K1R, int RNG>
-__global__ void __launch_bounds__(256, MODE == MODE_SMEM ? 1 : 2) drive_kernel(DriveArgs<T> p) {
+__global__ void __maxnreg__((UpdRegs<MODE, NS, K1R>::v)) drive_kernel(DriveArgs<T> p) {
   extern __shared__ __align__(16) unsigned char smem[];
   T *sig_s = reinterpret_cast<T *>(smem);
   load_table(sig_s, p.sig);
@@ -780,7 +790,8 @@ template <int NS>
 static int update_f2s(UpdateArgs<float> a, cudaStream_t st) {
   constexpr int NCH = (NS + 1) / 2;
   const bool hot = snapshot_mode(a.mv);
-  const bool staged = prefer_staged(update_windows_kernel<float, MODE_F2S, NS, NCH, 16, false>,
+  const char *force = std::getenv("SGNS_UPDATE_BODY");  // experiments: "g" / "s" force F2G / F2S
+  const bool staged = force ? force[0] == 's' : prefer_staged(update_windows_kernel<float, MODE_F2S, NS, NCH, 16, false>,
                                     update_windows_kernel<float, MODE_F2G, NS, NCH, 8, false>,
                                     slab_layout(MODE_F2S, 4, a.mv.ld, a.mcap, a.k1, 0).total,
                                     slab_layout(MODE_F2G, 4, a.mv.ld, a.mcap, a.k1, 0).total);

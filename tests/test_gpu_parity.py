@@ -219,16 +219,20 @@ def test_disjoint_windows_equal_sequential(dtype, D, k):
         assert bad_rows <= flips * 16, (bad_rows, flips)
 
 
-@pytest.mark.parametrize("dtype,D,k", [("f64", 300, 5), ("f32", 300, 5), ("f32", 100, 12),
-                                       ("f32", 64, 7), ("f32", 100, 5), ("f32", 300, 15),
-                                       ("f32", 200, 10)])
-def test_snapshot_conflicting_windows(dtype, D, k):
+@pytest.mark.parametrize("dtype,D,k,body", [("f64", 300, 5, ""), ("f32", 300, 5, ""), ("f32", 100, 12, ""),
+                                            ("f32", 64, 7, ""), ("f32", 100, 5, ""), ("f32", 300, 15, ""),
+                                            ("f32", 200, 10, ""), ("f32", 300, 9, ""), ("f32", 300, 15, "s"),
+                                            ("f32", 100, 12, "g"), ("f32", 300, 10, "s")])
+def test_snapshot_conflicting_windows(dtype, D, k, body, monkeypatch):
     """P3: Zipf-conflicting windows in snapshot mode == snapshot + sum of per-window deltas.
 
     float32 snapshot mode sums the hottest rows per warp before one scatter: rows [0, 8) of
     both matrices in shared memory where it fits (d = 64, 100, 200), row 0 of M_in in
-    registers otherwise (d = 300); K = 10 / 15 at d >= 200 take the two-register-group body.
+    registers otherwise (d = 300).  8 < K + 1 <= 16 takes the two-register-group body (F2G)
+    or the all-staged one (F2S), as the launcher chooses ("") or forced ("g" / "s").
     Zipf(1.3) puts id 0 in ~30% of the slots here."""
+    if body:
+        monkeypatch.setenv("SGNS_UPDATE_BODY", body)
     P, O = _pkg(), _oracle()
     from paper_1604_04661_b200.kernel_batched import DeviceWindowBatch, WindowBatch
     from paper_1604_04661_b200.model import DeviceModel, SIGMOID_TABLE_F32, SIGMOID_TABLE_F64
