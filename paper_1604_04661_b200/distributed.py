@@ -133,9 +133,12 @@ class Transport:
 
 
 def _coalescing(dist, group, device):
-    """ncclGroupStart/End around the enclosed collectives (torch's coalescing manager)."""
+    """ncclGroupStart/End around the enclosed collectives (torch's coalescing manager).
+    async_ops=False: on exit the group's work is waited, i.e. the current CUDA stream is
+    made to wait for NCCL's, so the next training launch cannot overlap the average (with
+    async_ops=True torch leaves that wait to the caller)."""
     from torch.distributed.distributed_c10d import _coalescing_manager
-    return _coalescing_manager(group=group, device=device, async_ops=True)
+    return _coalescing_manager(group=group, device=device, async_ops=False)
 
 
 class NcclTransport(Transport):
