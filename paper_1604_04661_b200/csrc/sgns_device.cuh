@@ -530,6 +530,58 @@ __device__ __forceinline__ void f2_dc(const ModelView<float> &mv, const F2Shape<
   __syncwarp();
 }
 
+// dC input-outer: NS x K1R float2 accumulators in registers (the caller's C registers
+// are dead by now), each staged row slot and error row read once
+template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT = false>
+__device__ __forceinline__ void f2_dc_io(const ModelView<float> &mv, const F2Shape<NS, NCH> &sh,
+                                         const uint32_t *off_s, int m, int k1, const float *rows_s,
+                                         const float *e_s, HotSink<NS> *hot = nullptr) {
+  auto kk_ok = [&](int k) { return EXACT_K || k < k1; };
+  float *out_dst_l = mv.out_dst + 2 * sh.lane;
+  float2 acc[NS][K1R];
+#pragma unroll
+  for (int j = 0; j < NS; ++j)
+#pragma unroll
+    for (int k = 0; k < K1R; ++k) acc[j][k] = f2zero();
+  const float *ap = rows_s + 2 * sh.lane;
+  const float *ep = e_s;
+  for (int i = 0; i < m; ++i, ap += sh.ld, ep += 8) {
+    const float4 e03 = *reinterpret_cast<const float4 *>(ep);
+    const float4 e47 = *reinterpret_cast<const float4 *>(ep + 4);
+    const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const float2 a0 = sh.slot_ok(j) ? *reinterpret_cast<const float2 *>(ap + 64 * j) : f2zero();
+#pragma unroll
+      for (int k = 0; k < K1R; ++k)
+        if (kk_ok(k)) acc[j][k] = __ffma2_rn(make_float2(ev[k], ev[k]), a0, acc[j][k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < K1R; ++k) {
+    if (!kk_ok(k)) continue;
+    const uint32_t ro = off_s[m + k];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      if (!sh.slot_ok(j)) continue;
+      if (HOT && ro < hot->out_lim) {
+        float2 *q = reinterpret_cast<float2 *>(hot->out_s + ro + 2 * (sh.lane + 32 * j));
+        *q = __fadd2_rn(*q, acc[j][k]);
+      } else {
+        atomicAdd(reinterpret_cast<float2 *>(out_dst_l + ro + 64 * j), acc[j][k]);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+#ifndef SGNS_F2_DC_IOUTER
+#define SGNS_F2_DC_IOUTER 1
+#endif
+#ifndef SGNS_F2G_DC_IOUTER
+#define SGNS_F2G_DC_IOUTER 0
+#endif
+
 template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT = false>
 __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, const uint32_t *off_s,
                                                  int m, int k1, float alpha, bool exact,
@@ -544,7 +596,11 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
   f2_load_c<NS, NCH, K1R, EXACT_K>(c, mv, sh, off_s + m, k1);
   f2_score_da<NS, NCH, K1R, EXACT_K, HOT>(c, mv, sh, off_s, m, k1, alpha, exact, sig_s, want_loss,
                                           loss_acc, cell_acc, rows_s, e_s, hot);
+#if SGNS_F2_DC_IOUTER
+  f2_dc_io<NS, NCH, K1R, EXACT_K, HOT>(mv, sh, off_s, m, k1, rows_s, e_s, &hot);
+#else
   f2_dc<NS, NCH, K1R, EXACT_K, HOT>(mv, sh, off_s, m, k1, rows_s, e_s, &hot);
+#endif
 }
 
 
@@ -570,11 +626,21 @@ __device__ __forceinline__ void window_update_f2g(const ModelView<float> &mv, co
   f2_score_da<NS, NCH, 8, false, HOT>(c, mv, sh, off_s, m, 8, alpha, exact, sig_s, want_loss,
                                       loss_acc, cell_acc, rows_s, e_s, hot, 0);
   float2 c2[K1R2][NS];
+#if SGNS_F2G_DC_IOUTER
+  // group 0's dC input-outer first (its C registers are dead), then group 1's rows: in
+  // place they are still gathered before this window's group-1 updates
+  f2_dc_io<NS, NCH, 8, false, HOT>(mv, sh, off_s, m, 8, rows_s, e_s, &hot);
+  f2_load_c<NS, NCH, K1R2, false>(c2, mv, sh, off_s + m + 8, k1 - 8);
+  f2_score_da<NS, NCH, K1R2, false, HOT>(c2, mv, sh, off_s, m, k1 - 8, alpha, exact, sig_s, want_loss,
+                                         loss_acc, cell_acc, rows_s, e_s, hot, 8);
+  f2_dc_io<NS, NCH, K1R2, false, HOT>(mv, sh, off_s + 8, m, k1 - 8, rows_s, e_s, &hot);
+#else
   f2_load_c<NS, NCH, K1R2, false>(c2, mv, sh, off_s + m + 8, k1 - 8);
   f2_dc<NS, NCH, 8, false, HOT>(mv, sh, off_s, m, 8, rows_s, e_s, &hot);
   f2_score_da<NS, NCH, K1R2, false, HOT>(c2, mv, sh, off_s, m, k1 - 8, alpha, exact, sig_s, want_loss,
                                          loss_acc, cell_acc, rows_s, e_s, hot, 8);
   f2_dc<NS, NCH, K1R2, false, HOT>(mv, sh, off_s + 8, m, k1 - 8, rows_s, e_s, &hot);
+#endif
 }
 
 // float32, 8 < k1 <= 16, d <= 512: like window_update_f2 but the k1 output rows stay in

@@ -1,6 +1,6 @@
-// sgns_fast.cuh -- production driver: Philox draws, dynamic sentence claiming and a
-// two-stage software pipeline across windows (float32, d <= 512, K + 1 <= 16: one warp
-// per worker up to K + 1 = 8, a pair of warps above).
+// sgns_fast.cuh -- production driver: Philox draws, dynamic sentence claiming and
+// negatives drawn one window ahead (float32, d <= 512, K + 1 <= 16: one warp per worker up
+// to K + 1 = 8, a pair of warps above).
 //
 // Differences from drive_kernel (the reference-stream driver), all invisible to the
 // update math:
@@ -11,11 +11,10 @@
 //  * alpha of a sentence is computed from its exact words-read position
 //    (update_alpha, trainer.py:122-132) instead of a racy shared counter.
 //  * the loss proxy samples every loss_every-th sentence (uniform over progress).
-//  * pipeline: the negatives of window u+1 are drawn (Philox + alias loads in flight)
-//    before window u is computed, and u+1's output rows are loaded into registers as
-//    soon as u's dA loop no longer needs C -- i.e. during u's dC pass.  If u and u+1
-//    share an output row, u's dC is added to the prefetched copy, so every window still
-//    sees its worker's previous updates exactly (the reference's per-thread order).
+//  * the negatives of window u+1 are drawn (Philox + alias loads in flight) before window
+//    u is computed; u+1's output rows are loaded right after u's dC scatter and so read
+//    it (same-thread order), so every window sees its worker's previous updates exactly,
+//    as a reference thread's does; their latency overlaps u+1's input-row gather.
 #pragma once
 
 #include "sgns_device.cuh"
@@ -192,10 +191,8 @@ template <int NS, int K1R> struct FastRegs {
 // rows, and scatter their own dC rows and their partial dA_i = sum over their outputs.
 // Two pair barriers per window keep the worker's order exact: after both copies of the
 // window's rows are staged (no scatter of the window starts before both warps read its
-// rows) and after both warps' scatters (the next window's gathers see both).  A prefetched
-// output row of the next window that the OTHER warp updates in this window is reloaded
-// after the second barrier; rows shared within a warp are patched as in the single-warp
-// form.  Leader warp (r = 0) alone claims sentences, counts, traces and marks rows.
+// rows) and after both warps' scatters (the next window's gathers and output-row loads
+// see both).  The leader warp (r = 0) alone claims sentences, counts, traces and marks rows.
 __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
 template <int NS, int NCH, int K1R, bool EXACT_K, bool FULL, bool PAIR = false>
@@ -490,9 +487,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
             if (slot_ok(j)) atomicAdd(reinterpret_cast<float2 *>(dst + 64 * j), d[j]);
         }
       }
-      // C registers are free: finish u+1's negatives and start loading its output rows
-      // bit (8 k + k') of lo_bits (k < 4) / hi_bits (k >= 4): out(u)[k] == out(u+1)[k']
-      unsigned lo_bits = 0, hi_bits = 0, cross_bits = 0;
+      // u+1's inputs, target and negatives (its candidates' alias loads were in flight)
       if (have) {
         for (int r = lane; r < nx.mc; r += 32) {
           const int q = nx.start + r;
@@ -503,78 +498,53 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
         select_negatives(p, cand_n, tok_n, ep, nx.ch, target, ids_n, nx.mc, lane);
         __syncwarp();
         for (int r = lane; r < nx.mc + k1; r += 32) off_n[r] = (uint32_t)ids_n[r] * (uint32_t)ld;
-        const int kq = lane & 7, ka = lane >> 3, kb = 4 + (lane >> 3);
-        const bool h1 = ka < kown && kq < kown && ids_s[m + kbase + ka] == ids_n[nx.mc + kbase + kq];
-        const bool h2 = kb < kown && kq < kown && ids_s[m + kbase + kb] == ids_n[nx.mc + kbase + kq];
-        lo_bits = __ballot_sync(0xffffffffu, h1);
-        hi_bits = __ballot_sync(0xffffffffu, h2);
-        if (PAIR) {
-          // bit kq: this warp's output kq of u+1 is a row the OTHER warp updates in u
-          const int obase = lead ? K1R : 0, oown = k1 - kown;
-          bool x = false;
-          if (lane < kown)
-            for (int o = 0; o < oown; ++o) x |= ids_n[nx.mc + kbase + lane] == ids_s[m + obase + o];
-          cross_bits = __ballot_sync(0xffffffffu, x);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < K1R; ++k) {
-          const float *src = out_src_l + off_n[nx.mc + kbase + (kk_ok(k) ? k : 0)];
-#pragma unroll
-          for (int j = 0; j < NS; ++j)
-            c_reg[k][j] = (kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 64 * j) : f2zero();
-        }
       }
       __syncwarp();
-      // dC_k = sum_i (alpha err_ik) A_i, column-outer; patch u+1's prefetched copies.
-      uint32_t orow[K1R];  // 32-bit row offsets: one IMAD.WIDE per scatter, 6 registers
+      // dC_k = sum_i (alpha err_ik) A_i, input-outer: u's C registers are dead once dA is
+      // out, so they hold the NS x K1R accumulators; each staged row slot and each error row
+      // is read once, and the NS x K1R FFMA2 chains are independent.  u+1's output rows are
+      // loaded after u's scatters (and, in pairs, after the pair barrier), so they read them:
+      // no patching, and their latency overlaps u+1's input-row gather.
+      {
+        uint32_t orow[K1R];
 #pragma unroll
-      for (int k = 0; k < K1R; ++k) orow[k] = off_s[m + kbase + (kk_ok(k) ? k : 0)];
+        for (int k = 0; k < K1R; ++k) orow[k] = off_s[m + kbase + (kk_ok(k) ? k : 0)];
+        float2 acc[NS][K1R];
 #pragma unroll
-      for (int j = 0; j < NS; ++j) {
-        if (!slot_ok(j)) continue;
-        const int col = 2 * (lane + 32 * j);
-        float2 acc[K1R];
+        for (int j = 0; j < NS; ++j)
 #pragma unroll
-        for (int k = 0; k < K1R; ++k) acc[k] = f2zero();
-        const float *ap = rows_s + col;
+          for (int k = 0; k < K1R; ++k) acc[j][k] = f2zero();
+        const float *ap = rows_s + 2 * lane;
         const float *ep = e_s;
         for (int i = 0; i < m; ++i, ap += ld, ep += 8) {
-          const float2 a0 = *reinterpret_cast<const float2 *>(ap);
           const float4 e03 = *reinterpret_cast<const float4 *>(ep);
           const float4 e47 = *reinterpret_cast<const float4 *>(ep + 4);
           const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
 #pragma unroll
-          for (int k = 0; k < K1R; ++k)
-            if (kk_ok(k)) acc[k] = __ffma2_rn(make_float2(ev[k], ev[k]), a0, acc[k]);
-        }
+          for (int j = 0; j < NS; ++j) {
+            const float2 a0 = slot_ok(j) ? *reinterpret_cast<const float2 *>(ap + 64 * j) : f2zero();
 #pragma unroll
-        for (int k = 0; k < K1R; ++k)
-          if (kk_ok(k)) atomicAdd(reinterpret_cast<float2 *>(out_dst_l + orow[k] + 64 * j), acc[k]);
-        if (lo_bits | hi_bits) {
-#pragma unroll
-          for (int k = 0; k < K1R; ++k) {
-            const unsigned row = k < 4 ? (lo_bits >> (8 * k)) & 0xFFu : (hi_bits >> (8 * (k - 4))) & 0xFFu;
-            if (row) {
-#pragma unroll
-              for (int kq = 0; kq < K1R; ++kq)
-                if (row & (1u << kq)) c_reg[kq][j] = __fadd2_rn(c_reg[kq][j], acc[k]);
-            }
+            for (int k = 0; k < K1R; ++k)
+              if (kk_ok(k)) acc[j][k] = __ffma2_rn(make_float2(ev[k], ev[k]), a0, acc[j][k]);
           }
         }
+#pragma unroll
+        for (int j = 0; j < NS; ++j)
+#pragma unroll
+          for (int k = 0; k < K1R; ++k)
+            if (kk_ok(k) && slot_ok(j)) atomicAdd(reinterpret_cast<float2 *>(out_dst_l + orow[k] + 64 * j), acc[j][k]);
       }
       __syncwarp();
-      if (PAIR) {
-        pair_bar(bar_id);  // both warps' scatters of u precede the gathers of u+1
-        if (cross_bits) {  // reload rows the other warp updated in u (its dC is now visible)
+      if (PAIR) pair_bar(bar_id);  // both warps' scatters of u precede every read of u+1
+      // (assigned on every path, so u's C is dead across the dC pass above)
+      {
+        const int nmc = have ? nx.mc : 0;
 #pragma unroll
-          for (int k = 0; k < K1R; ++k) {
-            if (!(cross_bits & (1u << k))) continue;
-            const float *src = out_src_l + off_n[nx.mc + kbase + k];
+        for (int k = 0; k < K1R; ++k) {
+          const float *src = out_src_l + off_n[nmc + kbase + (kk_ok(k) ? k : 0)];
 #pragma unroll
-            for (int j = 0; j < NS; ++j)
-              if (slot_ok(j)) c_reg[k][j] = ld_cg_f2(src + 64 * j);
-          }
+          for (int j = 0; j < NS; ++j)
+            c_reg[k][j] = (have && kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 64 * j) : f2zero();
         }
       }
       if (have) {
