@@ -575,12 +575,6 @@ __device__ __forceinline__ void f2_dc_io(const ModelView<float> &mv, const F2Sha
   __syncwarp();
 }
 
-#ifndef SGNS_F2_DC_IOUTER
-#define SGNS_F2_DC_IOUTER 1
-#endif
-#ifndef SGNS_F2G_DC_IOUTER
-#define SGNS_F2G_DC_IOUTER 0
-#endif
 
 template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT = false>
 __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, const uint32_t *off_s,
@@ -596,11 +590,10 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
   f2_load_c<NS, NCH, K1R, EXACT_K>(c, mv, sh, off_s + m, k1);
   f2_score_da<NS, NCH, K1R, EXACT_K, HOT>(c, mv, sh, off_s, m, k1, alpha, exact, sig_s, want_loss,
                                           loss_acc, cell_acc, rows_s, e_s, hot);
-#if SGNS_F2_DC_IOUTER
-  f2_dc_io<NS, NCH, K1R, EXACT_K, HOT>(mv, sh, off_s, m, k1, rows_s, e_s, &hot);
-#else
-  f2_dc<NS, NCH, K1R, EXACT_K, HOT>(mv, sh, off_s, m, k1, rows_s, e_s, &hot);
-#endif
+  // input-outer dC (C registers dead) up to 12 inputs; long windows (w = 10) measured
+  // faster column-outer (configs[1]: 0.61 vs 0.56)
+  if (m <= 12) f2_dc_io<NS, NCH, K1R, EXACT_K, HOT>(mv, sh, off_s, m, k1, rows_s, e_s, &hot);
+  else f2_dc<NS, NCH, K1R, EXACT_K, HOT>(mv, sh, off_s, m, k1, rows_s, e_s, &hot);
 }
 
 
@@ -626,21 +619,22 @@ __device__ __forceinline__ void window_update_f2g(const ModelView<float> &mv, co
   f2_score_da<NS, NCH, 8, false, HOT>(c, mv, sh, off_s, m, 8, alpha, exact, sig_s, want_loss,
                                       loss_acc, cell_acc, rows_s, e_s, hot, 0);
   float2 c2[K1R2][NS];
-#if SGNS_F2G_DC_IOUTER
-  // group 0's dC input-outer first (its C registers are dead), then group 1's rows: in
-  // place they are still gathered before this window's group-1 updates
-  f2_dc_io<NS, NCH, 8, false, HOT>(mv, sh, off_s, m, 8, rows_s, e_s, &hot);
-  f2_load_c<NS, NCH, K1R2, false>(c2, mv, sh, off_s + m + 8, k1 - 8);
-  f2_score_da<NS, NCH, K1R2, false, HOT>(c2, mv, sh, off_s, m, k1 - 8, alpha, exact, sig_s, want_loss,
-                                         loss_acc, cell_acc, rows_s, e_s, hot, 8);
-  f2_dc_io<NS, NCH, K1R2, false, HOT>(mv, sh, off_s + 8, m, k1 - 8, rows_s, e_s, &hot);
-#else
+  if (mv.out_src != mv.out_dst && m <= 12) {
+    // snapshot mode: group 0's dC input-outer first (its C registers are dead), then group
+    // 1's rows -- they come from the unchanged snapshot, so the order does not matter
+    f2_dc_io<NS, NCH, 8, false, HOT>(mv, sh, off_s, m, 8, rows_s, e_s, &hot);
+    f2_load_c<NS, NCH, K1R2, false>(c2, mv, sh, off_s + m + 8, k1 - 8);
+    f2_score_da<NS, NCH, K1R2, false, HOT>(c2, mv, sh, off_s, m, k1 - 8, alpha, exact, sig_s, want_loss,
+                                           loss_acc, cell_acc, rows_s, e_s, hot, 8);
+    f2_dc_io<NS, NCH, K1R2, false, HOT>(mv, sh, off_s + 8, m, k1 - 8, rows_s, e_s, &hot);
+    return;
+  }
+  // in place: group 1's rows are gathered before group 0's dC is scattered
   f2_load_c<NS, NCH, K1R2, false>(c2, mv, sh, off_s + m + 8, k1 - 8);
   f2_dc<NS, NCH, 8, false, HOT>(mv, sh, off_s, m, 8, rows_s, e_s, &hot);
   f2_score_da<NS, NCH, K1R2, false, HOT>(c2, mv, sh, off_s, m, k1 - 8, alpha, exact, sig_s, want_loss,
                                          loss_acc, cell_acc, rows_s, e_s, hot, 8);
   f2_dc<NS, NCH, K1R2, false, HOT>(mv, sh, off_s + 8, m, k1 - 8, rows_s, e_s, &hot);
-#endif
 }
 
 // float32, 8 < k1 <= 16, d <= 512: like window_update_f2 but the k1 output rows stay in
