@@ -6,7 +6,7 @@
 //    memory by 16-byte cp.async, output rows loaded straight into registers, packed
 //    FFMA2 math on a float2 column map, a transposed butterfly reducing two inputs'
 //    scores at once, dA and dC scattered with red.global.add.v2.f32.  The production
-//    driver (sgns_fast.cuh) inlines the same math inside its software pipeline.
+//    driver (sgns_fast.cuh) inlines the same math.
 //  * window_update (generic: float64, K + 1 > 8, d > 512): every row staged in shared
 //    memory, 16-byte vector math, scores reduced over 32 values.
 // Both gather every row before any write (the snapshot semantics of
@@ -328,8 +328,9 @@ __device__ __forceinline__ void window_update(const ModelView<T> &mv, const int 
 // 150 slots at d = 300 -> 5 slots on 22 lanes, 4 on 10 (94% balanced; the
 // 16-byte mapping wastes 22%).  All arithmetic is packed FFMA2 (Blackwell
 // f32x2), C lives in registers loaded straight from L2, only the m input rows
-// are staged in shared memory (cp.async, 16-byte), and dC is a column-outer
-// pass over the staged rows, so registers stay <= 128 and smem ~12 KB/warp.
+// are staged in shared memory (cp.async, 16-byte), and dC is a pass over the staged
+// rows whose accumulators take the C registers once dA is out (input-outer; column-outer
+// for long windows), so registers stay <= 128 for K + 1 <= 6 and smem ~12 KB/warp.
 __device__ __forceinline__ float2 f2zero() { return make_float2(0.f, 0.f); }
 __device__ __forceinline__ float2 ld_cg_f2(const float *p) {
   float2 v;
@@ -341,7 +342,8 @@ __device__ __forceinline__ float2 ld_cg_f2(const float *p) {
 //   f2_issue_a   input rows -> smem (16-byte cp.async)
 //   f2_load_c    output rows -> registers (8-byte L2 loads)
 //   f2_score_da  wait for the rows; scores, errors (to e_s), dA scattered
-//   f2_dc        dC_k = sum_i (alpha err_ik) A_i, column-outer over the staged rows
+//   f2_dc_io     dC_k = sum_i (alpha err_ik) A_i, input-outer, NS x K1R accumulators
+//   f2_dc        the same sum column-outer (windows of more than 12 inputs)
 template <int NS, int NCH> struct F2Shape {
   int ld, nvec, nslot, lane;
   __device__ F2Shape(const ModelView<float> &mv, int lane_)
