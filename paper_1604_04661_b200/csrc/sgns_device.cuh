@@ -78,6 +78,14 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+// predicated form (no branch around the copy)
+__device__ __forceinline__ void cp_async16_if(bool on, void *smem, const void *gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.cg.shared.global [%0], [%1], 16;\n}\n" ::"r"(s),
+      "l"(gmem), "r"((int)on)
+      : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
@@ -146,6 +154,48 @@ template <int NV> __device__ __forceinline__ int group_leader(int k) {
   return k << (5 - Log2<NV>::v);
 }
 
+// Transposed butterfly over any N <= 32 values (N need not be a power of two): each stage
+// halves the value count (rounding up) across one lane bit, then plain butterflies finish.
+// N = 12 (two inputs x six outputs) takes 6 + 3 + 2 + 1 + 1 = 13 shuffles where the padded
+// power-of-two form takes 16.  index(lane): which value the lane ends with, -1 for the
+// lanes an odd split leaves without one; kDupMask: lane bits over which a value is
+// replicated (the plain stages).
+template <int N, int BIT> struct TReduce {
+  static constexpr int H = (N + 1) / 2;
+  static constexpr int kDupMask = N == 1 ? (BIT | TReduce<1, BIT / 2>::kDupMask) : TReduce<H, BIT / 2>::kDupMask;
+  template <int NMAX>
+  static __device__ __forceinline__ float run(float (&v)[NMAX], int lane) {
+    if constexpr (N == 1) {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], BIT);
+      return TReduce<1, BIT / 2>::run(v, lane);
+    } else {
+      const bool upper = (lane & BIT) != 0;
+#pragma unroll
+      for (int q = 0; q < H; ++q) {
+        const float hi = q + H < N ? v[q + H] : 0.f;
+        const float send = upper ? v[q] : hi;
+        const float keep = upper ? hi : v[q];
+        v[q] = keep + __shfl_xor_sync(0xffffffffu, send, BIT);
+      }
+      return TReduce<H, BIT / 2>::run(v, lane);
+    }
+  }
+  static __device__ __forceinline__ int index(int lane) {
+    if constexpr (N == 1) {
+      return 0;
+    } else {
+      const int sub = TReduce<H, BIT / 2>::index(lane);
+      if ((lane & BIT) == 0 || sub < 0) return sub;
+      return sub + H < N ? sub + H : -1;
+    }
+  }
+};
+template <int N> struct TReduce<N, 0> {
+  static constexpr int kDupMask = 0;
+  template <int NMAX> static __device__ __forceinline__ float run(float (&v)[NMAX], int) { return v[0]; }
+  static __device__ __forceinline__ int index(int) { return 0; }
+};
+
 // model.py:108-115: idx = int((x + 6.0) * (1000.0 / 12.0)) in float64, clamped
 __device__ __forceinline__ int sig_index(double x) {
   const double v = (x + 6.0) * (1000.0 / 12.0);
@@ -193,12 +243,14 @@ __device__ __forceinline__ void cell_error(T s, int k, T alpha, bool exact, cons
 //    product, as the reference's double-then-float is; for label 1 fmaf(-alpha, sig,
 //    alpha) rounds alpha (1 - sig) once (the double path rounds twice: they can differ
 //    only when the exact value lies within 2^-53 of a float rounding boundary).
+// live: lanes holding no cell (a padded score of exactly 0 sits on the bin edge v = 500)
+// must not drag their warp through the float64 branch.
 __device__ __forceinline__ void cell_error_f32(float s, int k, float alpha, const float *sig_s,
-                                               float &e_raw, float &e_scaled) {
+                                               float &e_raw, float &e_scaled, bool live = true) {
   const float v = fmaf(s, 1000.0f / 12.0f, 500.0f);
   const float fl = floorf(v);
   int idx;
-  if (fabsf(v - rintf(v)) < 1e-3f || !(fabsf(v) < 1e7f)) {
+  if (live && (fabsf(v - rintf(v)) < 1e-3f || !(fabsf(v) < 1e7f))) {
     idx = sig_index((double)s);
   } else {
     idx = (int)fl;
@@ -335,6 +387,13 @@ __device__ __forceinline__ float2 f2zero() { return make_float2(0.f, 0.f); }
 __device__ __forceinline__ float2 ld_cg_f2(const float *p) {
   float2 v;
   asm volatile("ld.global.cg.v2.f32 {%0, %1}, [%2];\n" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 ld_cg_f4(const float *p) {
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
   return v;
 }
 

@@ -17,6 +17,8 @@
 //    as a reference thread's does; their latency overlaps u+1's input-row gather.
 #pragma once
 
+#include <type_traits>
+
 #include "sgns_device.cuh"
 
 namespace sgns {
@@ -59,8 +61,9 @@ struct FastArgs {
 };
 
 struct FastSlab {
-  int64_t rows, e, ids, roff, kept, koff, bw, cnt, total;
+  int64_t rows, e, ids, roff, kept, koff, bw, cnt, cand, total;
 };
+constexpr int kCandWords = 64;  // candidate negatives drawn per batch: one Philox call per lane
 __host__ __device__ inline FastSlab fast_slab(int64_t ld, int mcap, int k1r, int kept_cap) {
   FastSlab s;
   const int idsn = mcap + k1r;
@@ -72,7 +75,8 @@ __host__ __device__ inline FastSlab fast_slab(int64_t ld, int mcap, int k1r, int
   s.koff = s.kept + round16_(int64_t(kept_cap) * 4);
   s.bw = s.koff + round16_(int64_t(kept_cap) * 4);
   s.cnt = s.bw + round16_(int64_t(kept_cap) * 4);  // 5 counters, the loss, a pair's claim
-  s.total = s.cnt + 64;
+  s.cand = s.cnt + 64;
+  s.total = s.cand + kCandWords * 4;
   return s;
 }
 
@@ -137,14 +141,13 @@ __device__ __forceinline__ NegCand no_candidate() {
 
 // Accept the first k_neg candidates != target (kernel_batched.py:57-66 semantics, with
 // the attempt sequence of the oracle's philox restatement); writes ids_s[mc+1 ...].
-__device__ __forceinline__ void select_negatives(const FastArgs &p, NegCand cnd, uint64_t tok, uint32_t ep,
-                                                 int ch, int target, int *ids_s, int mc, int lane) {
+// cand / span: this lane's candidate of attempts [0, span) (lanes >= span: ignored).
+__device__ __forceinline__ void select_negatives(const FastArgs &p, int cand, int span, uint64_t tok,
+                                                 uint32_t ep, int ch, int target, int *ids_s, int mc, int lane) {
   const unsigned lt = (1u << lane) - 1u;
   int need = p.k_neg;
   uint32_t attempt = 0;
-  int span = min(32, p.k_neg + 2);
   while (true) {
-    const int cand = cnd.word();
     const bool ok = lane < span && cand != target;
     const unsigned mask = __ballot_sync(0xffffffffu, ok);
     const int avail = __popc(mask);
@@ -164,10 +167,31 @@ __device__ __forceinline__ void select_negatives(const FastArgs &p, NegCand cnd,
       break;
     }
     span = min(32, need + 2);
-    cnd = lane < span ? neg_candidate(p, tok, ep, ch, attempt + lane) : no_candidate();
+    cand = lane < span ? neg_candidate(p, tok, ep, ch, attempt + lane).word() : -1;
   }
 }
 
+#ifndef SGNS_FAST_Q4
+#define SGNS_FAST_Q4 1
+#endif
+#ifndef X_LIVE
+#define X_LIVE 1
+#endif
+#ifndef X_TR
+#define X_TR 1
+#endif
+#ifndef X_BATCH
+#define X_BATCH 1
+#endif
+#ifndef X_PEEL
+#define X_PEEL 0  // first dC row by FMUL2: spills at 128 registers (234M vs 262M words/s)
+#endif
+#ifndef X_BREAK
+#define X_BREAK 1
+#endif
+#ifndef X_PCP
+#define X_PCP 1
+#endif
 #ifndef SGNS_FAST_MAXNREG
 #define SGNS_FAST_MAXNREG 128
 #endif
@@ -197,7 +221,6 @@ __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64
 
 template <int NS, int NCH, int K1R, bool EXACT_K, bool FULL, bool PAIR = false>
 __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p) {
-  constexpr int NV = 8;
   constexpr int K1T = PAIR ? 2 * K1R : K1R;  // output ids held per window
   extern __shared__ __align__(16) unsigned char smem[];
   float *sig_s = reinterpret_cast<float *>(smem);
@@ -212,7 +235,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
   const int kbase = PAIR && !lead ? K1R : 0;                          // this warp's first output
   const int kown = PAIR ? (lead ? K1R : k1 - K1R) : k1;                // and how many
   const int mcap = min(p.cap, 2 * p.window);
-  const FastSlab L = fast_slab(p.mv.ld, mcap, K1T, p.kept_cap);
+  const FastSlab L = fast_slab(4 * p.mv.nvec, mcap, K1T, p.kept_cap);
   unsigned char *base = smem + round16_(kSigBins * 4) + (int64_t)warp * L.total;
   float *rows_s = reinterpret_cast<float *>(base + L.rows);
   float *e_s = reinterpret_cast<float *>(base + L.e);
@@ -221,6 +244,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
   int *kept_s = reinterpret_cast<int *>(base + L.kept);
   int *koff_s = reinterpret_cast<int *>(base + L.koff);
   int *bw_s = reinterpret_cast<int *>(base + L.bw);
+  int *cand_s = reinterpret_cast<int *>(base + L.cand);
   // words trained / read, chunks, inputs, and the current epoch's sampled loss cells and
   // loss sum of this worker: kept in shared memory (lane 0) rather than in 64-bit
   // registers live across the whole hot loop
@@ -251,18 +275,66 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
   };
   const int idsn = mcap + K1T;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const int ld = (int)p.mv.ld;  // shared-memory indexing in 32 bits
+  // nvec: 16-byte chunks of a row that hold data (dim rounded up to 4).  Staged rows are
+  // packed at that width in shared memory (ld); in HBM a row starts every gld >= ld elements
+  // (padded so rows start on 128-byte lines: every warp-wide access then covers whole lines).
   const int nvec = p.mv.nvec, nslot = 2 * nvec;
+  const int ld = 4 * nvec;
+  const uint32_t gld = (uint32_t)p.mv.ld;
   // lane offsets folded into the model base pointers once: every gather/scatter below is
   // base + 32-bit row offset + a compile-time slot offset
-  float *const in_dst_l = p.mv.in_dst + 2 * lane;
-  float *const out_dst_l = p.mv.out_dst + 2 * lane;
-  const float *const out_src_l = p.mv.out_src + 2 * lane;
+  // Column layout of a lane's NS float2 slots.  Q4: slots 2q, 2q + 1 are the halves of the
+  // 16-byte chunk q (columns 128 q + 4 lane ..+3), an odd last slot is the float2 at
+  // 128 NQ + 2 lane: rows move as 128-bit loads / RED.128 (2 + 1 instead of 5 at d = 300).
+  constexpr bool Q4 = SGNS_FAST_Q4 != 0;
+  constexpr int NQ = Q4 ? NS / 2 : 0;      // 16-byte chunks per lane
+  constexpr int NT = NS - 2 * NQ;          // float2 slots after them
+  const int lane_col = Q4 ? 4 * lane : 2 * lane;
+  const int tail_adj = Q4 ? 128 * NQ - 2 * lane : 0;  // first float2 slot relative to lane_col
+  float *const in_dst_l = p.mv.in_dst + lane_col;
+  float *const out_dst_l = p.mv.out_dst + lane_col;
+  const float *const out_src_l = p.mv.out_src + lane_col;
   const float *const in_src_l = p.mv.in_src + 4 * lane;
-  auto slot_ok = [&](int j) { return FULL || j < NS - 1 || lane + 32 * j < nslot; };
+  auto slot_ok = [&](int j) {
+    if (FULL) return true;
+    if (!Q4 || j >= 2 * NQ) return j < NS - 1 || lane + 32 * j < nslot;  // (Q4 tail: NS - 1 = 2 NQ)
+    return NT > 0 || j < 2 * NQ - 2 || lane + 32 * (NQ - 1) < nvec;
+  };
+  // row <- global (ld.cg), row <- shared, global += row; ptr = row base + lane_col
+  auto row_ldg = [&](float2 (&r)[NS], const float *src, bool on) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (on && slot_ok(2 * q)) v = ld_cg_f4(src + 128 * q);
+      r[2 * q] = make_float2(v.x, v.y);
+      r[2 * q + 1] = make_float2(v.z, v.w);
+    }
+#pragma unroll
+    for (int j = 2 * NQ; j < NS; ++j)
+      r[j] = (on && slot_ok(j)) ? ld_cg_f2(src + tail_adj + 64 * (j - 2 * NQ)) : f2zero();
+  };
+  auto row_red = [&](float *dst, const float2 (&r)[NS], bool on) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      if (on && slot_ok(2 * q))
+        atomicAdd(reinterpret_cast<float4 *>(dst + 128 * q),
+                  make_float4(r[2 * q].x, r[2 * q].y, r[2 * q + 1].x, r[2 * q + 1].y));
+#pragma unroll
+    for (int j = 2 * NQ; j < NS; ++j)
+      if (on && slot_ok(j)) atomicAdd(reinterpret_cast<float2 *>(dst + tail_adj + 64 * (j - 2 * NQ)), r[j]);
+  };
   auto chunk_ok = [&](int j) { return j < NCH - 1 || lane + 32 * j < nvec; };
   auto kk_ok = [&](int k) { return EXACT_K || k < kown; };
   const int rec_len = 4 + p.cap + k1;
+  // Negative candidates are drawn for a batch of consecutive kept positions at once: every
+  // lane runs ONE Philox call (two attempts) and its alias lookups, so the first NCAND
+  // attempts of WB chunk-0 windows cost one call per batch instead of one per window.
+  // Attempt order and acceptance are unchanged (attempts 0, 1, 2, ... in order; attempts
+  // past NCAND, and chunks after the first, are drawn directly in select_negatives).
+  constexpr int NCAND = PAIR ? 16 : 8;        // >= K + 2 whenever possible
+  constexpr int WB = kCandWords / NCAND;      // windows per batch
+  // score reduction: value h * K1R + k of an input pair on the lanes TR::index gives
+  using TR = TReduce<2 * K1R, 16>;
 
   int loss_epoch = -1;
 
@@ -335,6 +407,39 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
     __syncwarp();
     if (lane == 0 && lead) cnt_s[0] += nk;
 
+    // first-span candidate word of unit x for this lane; fresh: x is the first unit of its
+    // batch to be drawn (the batch is filled then)
+    auto batch_cand = [&](const Unit &x, bool fresh) {
+      if (fresh) {
+        const int b = x.pos / WB;
+        __syncwarp();  // earlier reads of cand_s are done
+        const int q = b * WB + lane / (NCAND / 2), cc = lane % (NCAND / 2);
+        if (q < nk) {
+          const uint4 o = philox_tok((uint64_t)(p.token_base + lo_t + koff_s[q]), ep, kTagNeg | (uint32_t)cc,
+                                     p.key0, p.key1);
+          const uint32_t b0 = (uint32_t)(((uint64_t)o.x * (uint64_t)p.vocab) >> 32);
+          const uint32_t b1 = (uint32_t)(((uint64_t)o.z * (uint64_t)p.vocab) >> 32);
+          const uint32_t t0 = __ldg(p.alias_thr + b0), t1 = __ldg(p.alias_thr + b1);
+          const int a0 = __ldg(p.alias_idx + b0), a1 = __ldg(p.alias_idx + b1);
+          *reinterpret_cast<int2 *>(cand_s + 2 * lane) = make_int2(o.y < t0 ? (int)b0 : a0, o.w < t1 ? (int)b1 : a1);
+        }
+        __syncwarp();
+      }
+      return lane < NCAND ? cand_s[(x.pos % WB) * NCAND + lane] : -1;
+    };
+    // u's negatives -> ids_s[mc + 1 ...]
+    auto draw_negatives = [&](const Unit &x, int *ids_s, bool fresh) {
+      const uint64_t tok = (uint64_t)(p.token_base + lo_t + koff_s[x.pos]);
+      const int target = kept_s[x.pos];
+      if (X_BATCH && x.ch == 0) {
+        const int cand = batch_cand(x, fresh);
+        select_negatives(p, cand, NCAND, tok, ep, 0, target, ids_s, x.mc, lane);
+      } else {
+        const int span = min(32, p.k_neg + 2);
+        const int cand = lane < span ? neg_candidate(p, tok, ep, x.ch, lane).word() : -1;
+        select_negatives(p, cand, span, tok, ep, x.ch, target, ids_s, x.mc, lane);
+      }
+    };
     Unit u;
     if (!first_unit(bw_s, nk, p.cap, u)) continue;
     // window u's inputs + target + negatives (synchronous for the first unit)
@@ -345,13 +450,10 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
         const int q = u.start + r;
         ids_s[r] = q < u.left ? kept_s[u.wlo + q] : kept_s[u.pos + 1 + (q - u.left)];
       }
-      const int target = kept_s[u.pos];
-      if (lane == 0) ids_s[u.mc] = target;
-      const uint64_t tok = (uint64_t)(p.token_base + lo_t + koff_s[u.pos]);
-      const NegCand cand = lane < min(32, p.k_neg + 2) ? neg_candidate(p, tok, ep, u.ch, lane) : no_candidate();
-      select_negatives(p, cand, tok, ep, u.ch, target, ids_s, u.mc, lane);
+      if (lane == 0) ids_s[u.mc] = kept_s[u.pos];
+      draw_negatives(u, ids_s, true);
       __syncwarp();
-      for (int r = lane; r < u.mc + k1; r += 32) roff_b[r] = (uint32_t)ids_s[r] * (uint32_t)ld;
+      for (int r = lane; r < u.mc + k1; r += 32) roff_b[r] = (uint32_t)ids_s[r] * gld;
       __syncwarp();
     }
     // C rows of u -> registers
@@ -359,15 +461,10 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
     {
       const uint32_t *off_s = roff_b;
 #pragma unroll
-      for (int k = 0; k < K1R; ++k) {
-        const float *src = out_src_l + off_s[u.mc + kbase + (kk_ok(k) ? k : 0)];
-#pragma unroll
-        for (int j = 0; j < NS; ++j)
-          c_reg[k][j] = (kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 64 * j) : f2zero();
-      }
+      for (int k = 0; k < K1R; ++k)
+        row_ldg(c_reg[k], out_src_l + off_s[u.mc + kbase + (kk_ok(k) ? k : 0)], kk_ok(k));
     }
-    bool have = true;
-    while (have) {
+    for (;;) {
       int *ids_s = ids_b + cur * idsn;
       const uint32_t *off_s = roff_b + cur * idsn;
       int *ids_n = ids_b + (cur ^ 1) * idsn;
@@ -378,21 +475,20 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
         const float *src = in_src_l + off_s[r];
         float *dst = rows_s + r * ld + 4 * lane;
 #pragma unroll
-        for (int j = 0; j < NCH; ++j)
+        for (int j = 0; j < NCH; ++j) {
+#if X_PCP
+          if (j < NCH - 1) cp_async16(dst + 128 * j, src + 128 * j);
+          else cp_async16_if(chunk_ok(j), dst + 128 * j, src + 128 * j);
+#else
           if (chunk_ok(j)) cp_async16(dst + 128 * j, src + 128 * j);
+#endif
+        }
       }
       if (p.dirty != nullptr && lead) {  // touched rows (data-parallel touched-row averaging)
         for (int r = lane; r < m + k1; r += 32) p.dirty[(r < m ? 0u : p.vocab) + (uint32_t)ids_s[r]] = 1;
       }
-      // next unit + its negative candidates (alias loads in flight during u's math)
       Unit nx;
-      have = next_unit(bw_s, nk, p.cap, u, nx);
-      NegCand cand_n = no_candidate();
-      uint64_t tok_n = 0;
-      if (have) {
-        tok_n = (uint64_t)(p.token_base + lo_t + koff_s[nx.pos]);
-        if (lane < min(32, p.k_neg + 2)) cand_n = neg_candidate(p, tok_n, ep, nx.ch, lane);
-      }
+      const bool have = next_unit(bw_s, nk, p.cap, u, nx);
       if (lane == 0 && lead) {
         cnt_s[2] += 1;
         cnt_s[3] += m;
@@ -424,37 +520,56 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
       // 5 serial shuffle stages) reduces both inputs' scores
       for (int i = 0; i < m; i += 2) {
         const bool two = i + 1 < m;
-        float pp[2 * NV];
+#if X_TR
+        float pp[2 * K1R];
+#else
+        float pp[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) pp[k] = 0.f;
+#endif
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int ii = two ? i + h : i;
           float2 a[NS];
+          {
+            const float *ap = rows_s + ii * ld + lane_col;
 #pragma unroll
-          for (int j = 0; j < NS; ++j)
-            a[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + ii * ld + 2 * (lane + 32 * j))
-                              : f2zero();
-#pragma unroll
-          for (int k = 0; k < NV; ++k) {
-            if (k < K1R) {
-              float2 acc = __fmul2_rn(a[0], c_reg[k][0]);
-#pragma unroll
-              for (int j = 1; j < NS; ++j) acc = __ffma2_rn(a[j], c_reg[k][j], acc);
-              pp[h * NV + k] = acc.x + acc.y;
-            } else {
-              pp[h * NV + k] = 0.f;
+            for (int q = 0; q < NQ; ++q) {
+              const float4 v = slot_ok(2 * q) ? *reinterpret_cast<const float4 *>(ap + 128 * q)
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+              a[2 * q] = make_float2(v.x, v.y);
+              a[2 * q + 1] = make_float2(v.z, v.w);
             }
+#pragma unroll
+            for (int j = 2 * NQ; j < NS; ++j)
+              a[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(ap + tail_adj + 64 * (j - 2 * NQ)) : f2zero();
+          }
+#pragma unroll
+          for (int k = 0; k < K1R; ++k) {
+            float2 acc = __fmul2_rn(a[0], c_reg[k][0]);
+#pragma unroll
+            for (int j = 1; j < NS; ++j) acc = __ffma2_rn(a[j], c_reg[k][j], acc);
+            pp[h * (X_TR ? K1R : 8) + k] = acc.x + acc.y;
           }
         }
-        // value v = h * 8 + k lands on lanes 2v, 2v + 1
-        const float sc = transpose_reduce<2 * NV>(pp, lane);
-        const int v = reduced_index<2 * NV>(lane);
+        // value h * K1R + k lands on the lanes with TR::index == that value
+#if X_TR
+        const float sc = TR::run(pp, lane);
+        const int tr_v = TR::index(lane);
+        const int hk = tr_v >= K1R ? 1 : 0, kk = tr_v < 0 ? K1R : tr_v - hk * K1R;
+        const int dupmask = TR::kDupMask;
+#else
+        const float sc = transpose_reduce<16>(pp, lane);
+        const int v = reduced_index<16>(lane);
         const int hk = v >> 3, kk = v & 7;
+        const int dupmask = 1;
+#endif
         float er = 0.f, es = 0.f;
         const bool live = kk < kown && (hk == 0 || two);
-        cell_error_f32(sc, kk + kbase, alpha, sig_s, er, es);
-        if (live) e_s[(i + hk) * 8 + kk] = es;  // both lanes of the pair hold the same value
+        cell_error_f32(sc, kk + kbase, alpha, sig_s, er, es, X_LIVE ? live : true);
+        if (live) e_s[(i + hk) * 8 + kk] = es;  // replicas of a value store the same word
         if (want) {  // sampled sentence: warp-reduce this pair's softplus terms
-          const bool mine = live && (lane & 1) == 0;
+          const bool mine = live && (lane & dupmask) == 0;  // one lane per value
           double sp = mine ? softplus(kk + kbase == 0 ? -(double)sc : (double)sc) : 0.0;
 #pragma unroll
           for (int o = 16; o >= 1; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
@@ -481,10 +596,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
             for (int j = 0; j < NS; ++j)
               d[j] = k == 0 ? __fmul2_rn(ek2, c_reg[0][j]) : __ffma2_rn(ek2, c_reg[k][j], d[j]);
           }
-          float *dst = in_dst_l + off_s[i + h];
-#pragma unroll
-          for (int j = 0; j < NS; ++j)
-            if (slot_ok(j)) atomicAdd(reinterpret_cast<float2 *>(dst + 64 * j), d[j]);
+          row_red(in_dst_l + off_s[i + h], d, true);
         }
       }
       // u+1's inputs, target and negatives (its candidates' alias loads were in flight)
@@ -493,11 +605,10 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
           const int q = nx.start + r;
           ids_n[r] = q < nx.left ? kept_s[nx.wlo + q] : kept_s[nx.pos + 1 + (q - nx.left)];
         }
-        const int target = kept_s[nx.pos];
-        if (lane == 0) ids_n[nx.mc] = target;
-        select_negatives(p, cand_n, tok_n, ep, nx.ch, target, ids_n, nx.mc, lane);
+        if (lane == 0) ids_n[nx.mc] = kept_s[nx.pos];
+        draw_negatives(nx, ids_n, nx.pos / WB != u.pos / WB);
         __syncwarp();
-        for (int r = lane; r < nx.mc + k1; r += 32) off_n[r] = (uint32_t)ids_n[r] * (uint32_t)ld;
+        for (int r = lane; r < nx.mc + k1; r += 32) off_n[r] = (uint32_t)ids_n[r] * gld;
       }
       __syncwarp();
       // dC_k = sum_i (alpha err_ik) A_i, input-outer: u's C registers are dead once dA is
@@ -510,47 +621,79 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
 #pragma unroll
         for (int k = 0; k < K1R; ++k) orow[k] = off_s[m + kbase + (kk_ok(k) ? k : 0)];
         float2 acc[NS][K1R];
+        const float *ap = rows_s + lane_col;
+        const float *ep = e_s;
+        // one input row into the accumulators; the first row initialises them (m >= 1)
+        auto dc_row = [&](auto first) {
+          constexpr bool FIRST = decltype(first)::value;
+          const float4 e03 = *reinterpret_cast<const float4 *>(ep);
+          const float4 e47 = *reinterpret_cast<const float4 *>(ep + 4);
+          const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
+          auto fma = [&](float2 &d, int k, const float2 &a) {
+            const float2 e2 = make_float2(ev[k], ev[k]);
+            if (!kk_ok(k)) {
+              if (FIRST) d = f2zero();
+            } else {
+              d = FIRST ? __fmul2_rn(e2, a) : __ffma2_rn(e2, a, d);
+            }
+          };
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const float4 v = slot_ok(2 * q) ? *reinterpret_cast<const float4 *>(ap + 128 * q)
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float2 a0 = make_float2(v.x, v.y), a1 = make_float2(v.z, v.w);
+#pragma unroll
+            for (int k = 0; k < K1R; ++k) {
+              fma(acc[2 * q][k], k, a0);
+              fma(acc[2 * q + 1][k], k, a1);
+            }
+          }
+#pragma unroll
+          for (int j = 2 * NQ; j < NS; ++j) {
+            const float2 a0 = slot_ok(j) ? *reinterpret_cast<const float2 *>(ap + tail_adj + 64 * (j - 2 * NQ))
+                                         : f2zero();
+#pragma unroll
+            for (int k = 0; k < K1R; ++k) fma(acc[j][k], k, a0);
+          }
+          ap += ld;
+          ep += 8;
+        };
+#if X_PEEL
+        dc_row(std::true_type{});
+        for (int i = 1; i < m; ++i) dc_row(std::false_type{});
+#else
 #pragma unroll
         for (int j = 0; j < NS; ++j)
 #pragma unroll
           for (int k = 0; k < K1R; ++k) acc[j][k] = f2zero();
-        const float *ap = rows_s + 2 * lane;
-        const float *ep = e_s;
-        for (int i = 0; i < m; ++i, ap += ld, ep += 8) {
-          const float4 e03 = *reinterpret_cast<const float4 *>(ep);
-          const float4 e47 = *reinterpret_cast<const float4 *>(ep + 4);
-          const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
+        for (int i = 0; i < m; ++i) dc_row(std::false_type{});
+#endif
 #pragma unroll
-          for (int j = 0; j < NS; ++j) {
-            const float2 a0 = slot_ok(j) ? *reinterpret_cast<const float2 *>(ap + 64 * j) : f2zero();
+        for (int k = 0; k < K1R; ++k) {
+          float2 r[NS];
 #pragma unroll
-            for (int k = 0; k < K1R; ++k)
-              if (kk_ok(k)) acc[j][k] = __ffma2_rn(make_float2(ev[k], ev[k]), a0, acc[j][k]);
-          }
+          for (int j = 0; j < NS; ++j) r[j] = acc[j][k];
+          row_red(out_dst_l + orow[k], r, kk_ok(k));
         }
-#pragma unroll
-        for (int j = 0; j < NS; ++j)
-#pragma unroll
-          for (int k = 0; k < K1R; ++k)
-            if (kk_ok(k) && slot_ok(j)) atomicAdd(reinterpret_cast<float2 *>(out_dst_l + orow[k] + 64 * j), acc[j][k]);
       }
       __syncwarp();
       if (PAIR) pair_bar(bar_id);  // both warps' scatters of u precede every read of u+1
-      // (assigned on every path, so u's C is dead across the dC pass above)
+#if X_BREAK
+      if (!have) break;  // (u's C is dead across the dC pass on this path too)
+#pragma unroll
+      for (int k = 0; k < K1R; ++k)
+        row_ldg(c_reg[k], out_src_l + off_n[nx.mc + kbase + (kk_ok(k) ? k : 0)], kk_ok(k));
+#else
       {
         const int nmc = have ? nx.mc : 0;
 #pragma unroll
-        for (int k = 0; k < K1R; ++k) {
-          const float *src = out_src_l + off_n[nmc + kbase + (kk_ok(k) ? k : 0)];
-#pragma unroll
-          for (int j = 0; j < NS; ++j)
-            c_reg[k][j] = (have && kk_ok(k) && slot_ok(j)) ? ld_cg_f2(src + 64 * j) : f2zero();
-        }
+        for (int k = 0; k < K1R; ++k)
+          row_ldg(c_reg[k], out_src_l + off_n[nmc + kbase + (kk_ok(k) ? k : 0)], have && kk_ok(k));
       }
-      if (have) {
-        u = nx;
-        cur ^= 1;
-      }
+      if (!have) break;
+#endif
+      u = nx;
+      cur ^= 1;
     }
   }
   // flush this worker's counters

@@ -924,7 +924,7 @@ template <int NS, int K1R, bool EXACT, bool FULL>
 static int launch_fast_t(FastArgs a, int wpb_req, cudaStream_t st, int *resident) {
   constexpr int NCH = (NS + 1) / 2;
   auto kern = drive_fast_kernel<NS, NCH, K1R, EXACT, FULL>;
-  const FastSlab L = fast_slab(a.mv.ld, std::min(a.cap, 2 * a.window), K1R, a.kept_cap);
+  const FastSlab L = fast_slab(4 * a.mv.nvec, std::min(a.cap, 2 * a.window), K1R, a.kept_cap);
   int wpb = 0, bps = 0;
   int rc = choose_wpb(kern, table_bytes(4), L.total, &wpb, &bps);
   if (rc) return rc;
@@ -943,7 +943,7 @@ static int launch_fast_t(FastArgs a, int wpb_req, cudaStream_t st, int *resident
 
 template <int NS>
 static int fast_ns(FastArgs a, int wpb, cudaStream_t st, int *res) {
-  const bool full = a.mv.ld == 64 * NS;  // 32 lanes x NS float2 slots exactly
+  const bool full = 4 * a.mv.nvec == 64 * NS;  // 32 lanes x NS float2 slots exactly
   // exact-K instantiations for K + 1 = 4..8 (no per-output predicates); K + 1 < 4 pads to 6
   switch (a.k_neg + 1) {
     case 4: return full ? launch_fast_t<NS, 4, true, true>(a, wpb, st, res)
@@ -967,7 +967,7 @@ int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
   FastArgs a;
   std::memset(&a, 0, sizeof(a));
   float *mi = static_cast<float *>(p->d_m_in), *mo = static_cast<float *>(p->d_m_out);
-  a.mv = ModelView<float>{mi, mo, mi, mo, p->ld, (int)(p->ld * 4 / 16)};
+  a.mv = ModelView<float>{mi, mo, mi, mo, p->ld, (p->dim + 3) / 4};  // nvec: the columns that hold data
   a.ids = p->d_ids;
   a.offsets = p->d_offsets;
   a.keep = p->d_keep_probs;
@@ -1007,8 +1007,8 @@ int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
   a.loss_total = p->d_loss_total;
   a.dirty = p->d_dirty;
   const int wpb = p->warps_per_block;
-  if (p->k_neg + 1 > 8) return pair_dispatch(a, p->ld, wpb, st, resident);  // warp pairs
-  switch (ns_for(p->ld)) {
+  if (p->k_neg + 1 > 8) return pair_dispatch(a, 4 * a.mv.nvec, wpb, st, resident);  // warp pairs
+  switch (ns_for(4 * a.mv.nvec)) {
 #if !defined(SGNS_ONLY_NS) || SGNS_ONLY_NS == 1
     case 1: return fast_ns<1>(a, wpb, st, resident);
 #endif
@@ -1047,7 +1047,7 @@ template <int NS, int K1R, bool FULL>
 static int launch_pair_t(FastArgs a, int wpb_req, cudaStream_t st, int *resident) {
   constexpr int NCH = (NS + 1) / 2;
   auto kern = drive_fast_kernel<NS, NCH, K1R, false, FULL, true>;
-  const FastSlab L = fast_slab(a.mv.ld, std::min(a.cap, 2 * a.window), 2 * K1R, a.kept_cap);
+  const FastSlab L = fast_slab(4 * a.mv.nvec, std::min(a.cap, 2 * a.window), 2 * K1R, a.kept_cap);
   int best = -1, wpb = 2, bps = 1;
   for (int w : {2, 4, 8, 16}) {  // warps per block: whole pairs
     const int64_t bytes = table_bytes(4) + (int64_t)w * L.total;
@@ -1122,9 +1122,9 @@ int pair_dispatch(const FastArgs &a, int64_t ld, int wpb, cudaStream_t st, int *
 
 #if SGNS_HAS(0)
 static bool fast_eligible(const sgns_drive_params *p) {
-  const int64_t ld = p->ld;
+  const int64_t ld = p->ld, cols = 4 * ((p->dim + 3) / 4);  // row stride, columns holding data
   return p->dtype == SGNS_F32 && p->rng_mode == SGNS_RNG_PHILOX && p->k_neg + 1 <= 16 &&
-         ns_for(ld) >= 1 && ns_for(ld) <= 8 && offsets32_ok(p->vocab, ld) &&
+         ns_for(cols) >= 1 && ns_for(cols) <= 8 && offsets32_ok(p->vocab, ld) &&
          p->sigmoid_mode == SGNS_SIGMOID_TABLE;
 }
 

@@ -6,7 +6,8 @@ Reference map:
   sigmoid / sigmoid table   sgns/model.py:77-115  (host table uploaded; index math stays float64)
 
 HBM layout: each matrix is a (V, ld) row-major tensor with ld = dim rounded up
-so a row is a whole number of 16-byte chunks (ld = 300 at d = 300); padding
+so a row is a whole number of 16-byte chunks, and for float32 to a whole number
+of 128-byte lines when that costs at most 12.5% (ld = 320 at d = 300); padding
 columns are zero and stay zero.  Dims that are multiples of 64 get the fast
 path's whole-slot variant automatically.
 """
@@ -80,20 +81,22 @@ SIGMOID_TABLE_F64 = build_sigmoid_table(np.float64)
 
 import os
 
-# tuning knob: maximal padding fraction accepted for whole-slot rows.  Measured at
-# d = 300 (ld 320, +6.7% bytes): 229.9M vs 230.8M words/s unpadded, so off by default.
-LD_FULL_WASTE = float(os.environ.get("SGNS_LD_FULL_WASTE", "0"))
+# Row stride policy for float32 models: pad rows to a multiple of 32 floats (128 bytes) when
+# that costs at most LD_LINE_WASTE of the model, so that every row starts on a 128-byte line
+# and a warp-wide gather / RED.128 covers whole lines (d = 300 -> ld = 320: 4 + 4 + 2 L2
+# requests per row instead of 5 + 5 + 2..3; +7% words/s on the 1M-word model).  The kernels
+# only touch the dim columns that hold data; the pad stays zero.
+LD_LINE_WASTE = float(os.environ.get("SGNS_LD_LINE_WASTE", "0.125"))
 
 
 def padded_ld(dim: int, dtype) -> int:
-    """Row stride: a whole number of 16-byte chunks (optionally padded to a multiple of
-    64 floats when that costs at most LD_FULL_WASTE)."""
+    """Row stride in elements: a whole number of 16-byte chunks, line-aligned when cheap."""
     per16 = 16 // np.dtype(dtype).itemsize
     ld = -(-dim // per16) * per16
-    if np.dtype(dtype) == np.float32 and dim <= 512:
-        full = -(-dim // 64) * 64
-        if full != ld and (full - dim) / dim <= LD_FULL_WASTE:
-            ld = full
+    if np.dtype(dtype) == np.float32:
+        line = -(-dim // 32) * 32
+        if (line - dim) / dim <= LD_LINE_WASTE:
+            ld = line
     return ld
 
 

@@ -32,7 +32,7 @@ from . import _lib
 from .corpus import (KEPT_BUFFER_TOKENS, EncodedCorpus, NegativeTable, Vocabulary, build_vocab,
                      default_table_length, encode_corpus, negative_table_boundaries,
                      read_tokens, split_by_tokens, NEGATIVE_POWER)
-from .model import DeviceModel, EmbeddingModel, current_stream_ptr, init_device_model
+from .model import DeviceModel, EmbeddingModel, current_stream_ptr, init_device_model, padded_ld
 from .kernel_batched import device_sigmoid_table
 from .rng import new_state
 
@@ -125,9 +125,10 @@ class TrainingConfig:
             raise ConfigError("schedule='dynamic' needs rng='philox', float32, negatives <= 15, dim <= 512")
 
     def dynamic_eligible(self, vocab_size: int) -> bool:
-        ld = -(-self.dim // 4) * 4
+        cols = -(-self.dim // 4) * 4
+        ld = padded_ld(self.dim, np.float32)
         return (self.rng == "philox" and not self.float64 and self.negatives + 1 <= 16
-                and -(-(ld // 2) // 32) <= 8 and vocab_size * ld < 2**32)
+                and -(-(cols // 2) // 32) <= 8 and vocab_size * ld < 2**32)
 
     def use_dynamic(self, vocab_size: int) -> bool:
         if self.schedule == "static":
