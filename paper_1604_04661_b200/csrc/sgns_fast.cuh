@@ -17,8 +17,6 @@
 //    as a reference thread's does; their latency overlaps u+1's input-row gather.
 #pragma once
 
-#include <type_traits>
-
 #include "sgns_device.cuh"
 
 namespace sgns {
@@ -60,6 +58,13 @@ struct FastArgs {
   uint8_t *dirty;              // optional touched-row map [2 * vocab]
 };
 
+// Shared-memory stride of a staged input row, in floats: the data columns rounded up to 32
+// bytes.  A 16-byte cp.async whose shared destination and global source differ in their
+// offset within a 32-byte sector makes L1 fetch one sector per LANE (32 per warp
+// instruction instead of 16; tools/probes/ldgsts_probe.cu), so staged rows keep the phase
+// of the 128-byte-aligned model rows.
+__host__ __device__ inline int fast_lds(int nvec) { return (4 * nvec + 7) & ~7; }
+
 struct FastSlab {
   int64_t rows, e, ids, roff, kept, koff, bw, cnt, cand, total;
 };
@@ -76,7 +81,7 @@ __host__ __device__ inline FastSlab fast_slab(int64_t ld, int mcap, int k1r, int
   s.bw = s.koff + round16_(int64_t(kept_cap) * 4);
   s.cnt = s.bw + round16_(int64_t(kept_cap) * 4);  // 5 counters, the loss, a pair's claim
   s.cand = s.cnt + 64;
-  s.total = s.cand + kCandWords * 4;
+  s.total = (s.cand + kCandWords * 4 + 31) & ~int64_t(31);  // slabs keep the 32-byte phase
   return s;
 }
 
@@ -171,27 +176,6 @@ __device__ __forceinline__ void select_negatives(const FastArgs &p, int cand, in
   }
 }
 
-#ifndef SGNS_FAST_Q4
-#define SGNS_FAST_Q4 1
-#endif
-#ifndef X_LIVE
-#define X_LIVE 1
-#endif
-#ifndef X_TR
-#define X_TR 1
-#endif
-#ifndef X_BATCH
-#define X_BATCH 1
-#endif
-#ifndef X_PEEL
-#define X_PEEL 0  // first dC row by FMUL2: spills at 128 registers (234M vs 262M words/s)
-#endif
-#ifndef X_BREAK
-#define X_BREAK 1
-#endif
-#ifndef X_PCP
-#define X_PCP 1
-#endif
 #ifndef SGNS_FAST_MAXNREG
 #define SGNS_FAST_MAXNREG 128
 #endif
@@ -222,7 +206,7 @@ __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64
 template <int NS, int NCH, int K1R, bool EXACT_K, bool FULL, bool PAIR = false>
 __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p) {
   constexpr int K1T = PAIR ? 2 * K1R : K1R;  // output ids held per window
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   float *sig_s = reinterpret_cast<float *>(smem);
   for (int i = threadIdx.x; i < kSigBins; i += blockDim.x) sig_s[i] = p.sig[i];
   __syncthreads();
@@ -235,7 +219,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
   const int kbase = PAIR && !lead ? K1R : 0;                          // this warp's first output
   const int kown = PAIR ? (lead ? K1R : k1 - K1R) : k1;                // and how many
   const int mcap = min(p.cap, 2 * p.window);
-  const FastSlab L = fast_slab(4 * p.mv.nvec, mcap, K1T, p.kept_cap);
+  const FastSlab L = fast_slab(fast_lds(p.mv.nvec), mcap, K1T, p.kept_cap);
   unsigned char *base = smem + round16_(kSigBins * 4) + (int64_t)warp * L.total;
   float *rows_s = reinterpret_cast<float *>(base + L.rows);
   float *e_s = reinterpret_cast<float *>(base + L.e);
@@ -276,28 +260,27 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
   const int idsn = mcap + K1T;
   const unsigned lt_mask = (1u << lane) - 1u;
   // nvec: 16-byte chunks of a row that hold data (dim rounded up to 4).  Staged rows are
-  // packed at that width in shared memory (ld); in HBM a row starts every gld >= ld elements
+  // packed at that width (rounded to 32 bytes, fast_lds) in shared memory (ld); in HBM a row starts every gld >= ld elements
   // (padded so rows start on 128-byte lines: every warp-wide access then covers whole lines).
   const int nvec = p.mv.nvec, nslot = 2 * nvec;
-  const int ld = 4 * nvec;
+  const int ld = fast_lds(nvec);
   const uint32_t gld = (uint32_t)p.mv.ld;
   // lane offsets folded into the model base pointers once: every gather/scatter below is
   // base + 32-bit row offset + a compile-time slot offset
-  // Column layout of a lane's NS float2 slots.  Q4: slots 2q, 2q + 1 are the halves of the
+  // Column layout of a lane's NS float2 slots: slots 2q, 2q + 1 are the halves of the
   // 16-byte chunk q (columns 128 q + 4 lane ..+3), an odd last slot is the float2 at
   // 128 NQ + 2 lane: rows move as 128-bit loads / RED.128 (2 + 1 instead of 5 at d = 300).
-  constexpr bool Q4 = SGNS_FAST_Q4 != 0;
-  constexpr int NQ = Q4 ? NS / 2 : 0;      // 16-byte chunks per lane
-  constexpr int NT = NS - 2 * NQ;          // float2 slots after them
-  const int lane_col = Q4 ? 4 * lane : 2 * lane;
-  const int tail_adj = Q4 ? 128 * NQ - 2 * lane : 0;  // first float2 slot relative to lane_col
+  constexpr int NQ = NS / 2;       // 16-byte chunks per lane
+  constexpr int NT = NS - 2 * NQ;  // float2 slot after them (0 or 1)
+  const int lane_col = 4 * lane;
+  const int tail_adj = 128 * NQ - 2 * lane;  // the float2 slot relative to lane_col
   float *const in_dst_l = p.mv.in_dst + lane_col;
   float *const out_dst_l = p.mv.out_dst + lane_col;
   const float *const out_src_l = p.mv.out_src + lane_col;
   const float *const in_src_l = p.mv.in_src + 4 * lane;
   auto slot_ok = [&](int j) {
     if (FULL) return true;
-    if (!Q4 || j >= 2 * NQ) return j < NS - 1 || lane + 32 * j < nslot;  // (Q4 tail: NS - 1 = 2 NQ)
+    if (j >= 2 * NQ) return lane + 32 * j < nslot;  // the float2 slot
     return NT > 0 || j < 2 * NQ - 2 || lane + 32 * (NQ - 1) < nvec;
   };
   // row <- global (ld.cg), row <- shared, global += row; ptr = row base + lane_col
@@ -431,7 +414,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
     auto draw_negatives = [&](const Unit &x, int *ids_s, bool fresh) {
       const uint64_t tok = (uint64_t)(p.token_base + lo_t + koff_s[x.pos]);
       const int target = kept_s[x.pos];
-      if (X_BATCH && x.ch == 0) {
+      if (x.ch == 0) {
         const int cand = batch_cand(x, fresh);
         select_negatives(p, cand, NCAND, tok, ep, 0, target, ids_s, x.mc, lane);
       } else {
@@ -476,12 +459,8 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
         float *dst = rows_s + r * ld + 4 * lane;
 #pragma unroll
         for (int j = 0; j < NCH; ++j) {
-#if X_PCP
           if (j < NCH - 1) cp_async16(dst + 128 * j, src + 128 * j);
           else cp_async16_if(chunk_ok(j), dst + 128 * j, src + 128 * j);
-#else
-          if (chunk_ok(j)) cp_async16(dst + 128 * j, src + 128 * j);
-#endif
         }
       }
       if (p.dirty != nullptr && lead) {  // touched rows (data-parallel touched-row averaging)
@@ -520,13 +499,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
       // 5 serial shuffle stages) reduces both inputs' scores
       for (int i = 0; i < m; i += 2) {
         const bool two = i + 1 < m;
-#if X_TR
         float pp[2 * K1R];
-#else
-        float pp[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) pp[k] = 0.f;
-#endif
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int ii = two ? i + h : i;
@@ -549,27 +522,19 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
             float2 acc = __fmul2_rn(a[0], c_reg[k][0]);
 #pragma unroll
             for (int j = 1; j < NS; ++j) acc = __ffma2_rn(a[j], c_reg[k][j], acc);
-            pp[h * (X_TR ? K1R : 8) + k] = acc.x + acc.y;
+            pp[h * K1R + k] = acc.x + acc.y;
           }
         }
         // value h * K1R + k lands on the lanes with TR::index == that value
-#if X_TR
         const float sc = TR::run(pp, lane);
         const int tr_v = TR::index(lane);
         const int hk = tr_v >= K1R ? 1 : 0, kk = tr_v < 0 ? K1R : tr_v - hk * K1R;
-        const int dupmask = TR::kDupMask;
-#else
-        const float sc = transpose_reduce<16>(pp, lane);
-        const int v = reduced_index<16>(lane);
-        const int hk = v >> 3, kk = v & 7;
-        const int dupmask = 1;
-#endif
         float er = 0.f, es = 0.f;
         const bool live = kk < kown && (hk == 0 || two);
-        cell_error_f32(sc, kk + kbase, alpha, sig_s, er, es, X_LIVE ? live : true);
+        cell_error_f32(sc, kk + kbase, alpha, sig_s, er, es, live);
         if (live) e_s[(i + hk) * 8 + kk] = es;  // replicas of a value store the same word
         if (want) {  // sampled sentence: warp-reduce this pair's softplus terms
-          const bool mine = live && (lane & dupmask) == 0;  // one lane per value
+          const bool mine = live && (lane & TR::kDupMask) == 0;  // one lane per value
           double sp = mine ? softplus(kk + kbase == 0 ? -(double)sc : (double)sc) : 0.0;
 #pragma unroll
           for (int o = 16; o >= 1; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
@@ -623,51 +588,35 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
         float2 acc[NS][K1R];
         const float *ap = rows_s + lane_col;
         const float *ep = e_s;
-        // one input row into the accumulators; the first row initialises them (m >= 1)
-        auto dc_row = [&](auto first) {
-          constexpr bool FIRST = decltype(first)::value;
+#pragma unroll
+        for (int j = 0; j < NS; ++j)
+#pragma unroll
+          for (int k = 0; k < K1R; ++k) acc[j][k] = f2zero();
+        // (peeling the first row to FMUL2 instead of zeroing the accumulators spills at 128
+        // registers: 234M vs 262M words/s)
+        for (int i = 0; i < m; ++i, ap += ld, ep += 8) {
           const float4 e03 = *reinterpret_cast<const float4 *>(ep);
           const float4 e47 = *reinterpret_cast<const float4 *>(ep + 4);
           const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
-          auto fma = [&](float2 &d, int k, const float2 &a) {
-            const float2 e2 = make_float2(ev[k], ev[k]);
-            if (!kk_ok(k)) {
-              if (FIRST) d = f2zero();
-            } else {
-              d = FIRST ? __fmul2_rn(e2, a) : __ffma2_rn(e2, a, d);
-            }
-          };
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
             const float4 v = slot_ok(2 * q) ? *reinterpret_cast<const float4 *>(ap + 128 * q)
                                             : make_float4(0.f, 0.f, 0.f, 0.f);
             const float2 a0 = make_float2(v.x, v.y), a1 = make_float2(v.z, v.w);
 #pragma unroll
-            for (int k = 0; k < K1R; ++k) {
-              fma(acc[2 * q][k], k, a0);
-              fma(acc[2 * q + 1][k], k, a1);
-            }
+            for (int k = 0; k < K1R; ++k)
+              if (kk_ok(k)) {
+                acc[2 * q][k] = __ffma2_rn(make_float2(ev[k], ev[k]), a0, acc[2 * q][k]);
+                acc[2 * q + 1][k] = __ffma2_rn(make_float2(ev[k], ev[k]), a1, acc[2 * q + 1][k]);
+              }
           }
+          if (NT > 0) {
+            const float2 a0 = slot_ok(2 * NQ) ? *reinterpret_cast<const float2 *>(ap + tail_adj) : f2zero();
 #pragma unroll
-          for (int j = 2 * NQ; j < NS; ++j) {
-            const float2 a0 = slot_ok(j) ? *reinterpret_cast<const float2 *>(ap + tail_adj + 64 * (j - 2 * NQ))
-                                         : f2zero();
-#pragma unroll
-            for (int k = 0; k < K1R; ++k) fma(acc[j][k], k, a0);
+            for (int k = 0; k < K1R; ++k)
+              if (kk_ok(k)) acc[NS - 1][k] = __ffma2_rn(make_float2(ev[k], ev[k]), a0, acc[NS - 1][k]);
           }
-          ap += ld;
-          ep += 8;
-        };
-#if X_PEEL
-        dc_row(std::true_type{});
-        for (int i = 1; i < m; ++i) dc_row(std::false_type{});
-#else
-#pragma unroll
-        for (int j = 0; j < NS; ++j)
-#pragma unroll
-          for (int k = 0; k < K1R; ++k) acc[j][k] = f2zero();
-        for (int i = 0; i < m; ++i) dc_row(std::false_type{});
-#endif
+        }
 #pragma unroll
         for (int k = 0; k < K1R; ++k) {
           float2 r[NS];
@@ -678,20 +627,10 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
       }
       __syncwarp();
       if (PAIR) pair_bar(bar_id);  // both warps' scatters of u precede every read of u+1
-#if X_BREAK
       if (!have) break;  // (u's C is dead across the dC pass on this path too)
 #pragma unroll
       for (int k = 0; k < K1R; ++k)
         row_ldg(c_reg[k], out_src_l + off_n[nx.mc + kbase + (kk_ok(k) ? k : 0)], kk_ok(k));
-#else
-      {
-        const int nmc = have ? nx.mc : 0;
-#pragma unroll
-        for (int k = 0; k < K1R; ++k)
-          row_ldg(c_reg[k], out_src_l + off_n[nmc + kbase + (kk_ok(k) ? k : 0)], have && kk_ok(k));
-      }
-      if (!have) break;
-#endif
       u = nx;
       cur ^= 1;
     }

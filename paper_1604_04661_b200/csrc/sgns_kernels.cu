@@ -35,7 +35,11 @@ namespace sgns {
 constexpr int kMaxSentence = 1024;
 constexpr int kMaxK1 = 32;
 
-__host__ __device__ inline int64_t round16(int64_t b) { return (b + 15) & ~int64_t(15); }
+// slab pieces start on 32-byte boundaries: a 16-byte cp.async whose shared destination and
+// global source differ in their offset within a 32-byte sector fetches one sector per lane
+// (tools/probes/ldgsts_probe.cu), so staged rows keep the sector phase of the model rows
+// whenever ld is a multiple of 32 bytes (model.py padded_ld)
+__host__ __device__ inline int64_t round32(int64_t b) { return (b + 31) & ~int64_t(31); }
 
 // shared-memory slab of one warp
 struct Slab {
@@ -50,19 +54,19 @@ __host__ __device__ inline Slab slab_layout(int mode, int64_t elem, int64_t ld, 
   Slab s;
   s.rows = 0;
   const bool a_only = mode == MODE_F2 || mode == MODE_F2G;  // only the input rows are staged
-  s.e = round16((int64_t)(a_only ? mcap : mcap + k1) * ld * elem);
+  s.e = round32((int64_t)(a_only ? mcap : mcap + k1) * ld * elem);
   // error rows: padded to 8 floats (F2, F2G per group), 16 (F2S), k1 (generic)
   const int erow = mode == MODE_F2S ? 16 : mode == MODE_F2G ? 8 : (k1 > 8 ? k1 : 8);
   // F2 / F2G keep only the scaled errors; the other bodies keep raw and scaled
-  s.ids = s.e + round16((int64_t)(a_only ? 1 : 2) * mcap * erow * elem);
-  s.roff = s.ids + round16((int64_t)(mcap + k1) * 4);
-  s.kept = s.roff + round16((int64_t)(mcap + k1) * 4);
-  s.off = s.kept + round16((int64_t)kept_cap * 4);
-  s.hot = s.off + round16((int64_t)kept_cap * 4);
-  s.total = s.hot + round16((int64_t)hot_rows * ld * elem);
+  s.ids = s.e + round32((int64_t)(a_only ? 1 : 2) * mcap * erow * elem);
+  s.roff = s.ids + round32((int64_t)(mcap + k1) * 4);
+  s.kept = s.roff + round32((int64_t)(mcap + k1) * 4);
+  s.off = s.kept + round32((int64_t)kept_cap * 4);
+  s.hot = s.off + round32((int64_t)kept_cap * 4);
+  s.total = s.hot + round32((int64_t)hot_rows * ld * elem);
   return s;
 }
-__host__ __device__ inline int64_t table_bytes(int64_t elem) { return round16(kSigBins * elem); }
+__host__ __device__ inline int64_t table_bytes(int64_t elem) { return round32(kSigBins * elem); }
 
 template <typename T>
 __device__ __forceinline__ void load_table(T *sig_s, const T *sig_g) {
@@ -146,7 +150,7 @@ template <int MODE, int NS, int K1R> struct UpdRegs {
 };
 template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT>
 __global__ void __maxnreg__((UpdRegs<MODE, NS, K1R>::v)) update_windows_kernel(UpdateArgs<T> p) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   T *sig_s = reinterpret_cast<T *>(smem);
   load_table(sig_s, p.sig);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -275,7 +279,7 @@ struct SmBatch {
 
 template <typename T, int MODE, int NS, int NCH, int K1R, int RNG>
 __global__ void __maxnreg__((UpdRegs<MODE, NS, K1R>::v)) drive_kernel(DriveArgs<T> p) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   T *sig_s = reinterpret_cast<T *>(smem);
   load_table(sig_s, p.sig);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -924,7 +928,7 @@ template <int NS, int K1R, bool EXACT, bool FULL>
 static int launch_fast_t(FastArgs a, int wpb_req, cudaStream_t st, int *resident) {
   constexpr int NCH = (NS + 1) / 2;
   auto kern = drive_fast_kernel<NS, NCH, K1R, EXACT, FULL>;
-  const FastSlab L = fast_slab(4 * a.mv.nvec, std::min(a.cap, 2 * a.window), K1R, a.kept_cap);
+  const FastSlab L = fast_slab(fast_lds(a.mv.nvec), std::min(a.cap, 2 * a.window), K1R, a.kept_cap);
   int wpb = 0, bps = 0;
   int rc = choose_wpb(kern, table_bytes(4), L.total, &wpb, &bps);
   if (rc) return rc;
@@ -1047,7 +1051,7 @@ template <int NS, int K1R, bool FULL>
 static int launch_pair_t(FastArgs a, int wpb_req, cudaStream_t st, int *resident) {
   constexpr int NCH = (NS + 1) / 2;
   auto kern = drive_fast_kernel<NS, NCH, K1R, false, FULL, true>;
-  const FastSlab L = fast_slab(4 * a.mv.nvec, std::min(a.cap, 2 * a.window), 2 * K1R, a.kept_cap);
+  const FastSlab L = fast_slab(fast_lds(a.mv.nvec), std::min(a.cap, 2 * a.window), 2 * K1R, a.kept_cap);
   int best = -1, wpb = 2, bps = 1;
   for (int w : {2, 4, 8, 16}) {  // warps per block: whole pairs
     const int64_t bytes = table_bytes(4) + (int64_t)w * L.total;

@@ -6,7 +6,7 @@ Reference map:
   sigmoid / sigmoid table   sgns/model.py:77-115  (host table uploaded; index math stays float64)
 
 HBM layout: each matrix is a (V, ld) row-major tensor with ld = dim rounded up
-so a row is a whole number of 16-byte chunks, and for float32 to a whole number
+so a row is a whole number of 32-byte sectors, and for float32 a whole number
 of 128-byte lines when that costs at most 12.5% (ld = 320 at d = 300); padding
 columns are zero and stay zero.  Dims that are multiples of 64 get the fast
 path's whole-slot variant automatically.
@@ -81,18 +81,20 @@ SIGMOID_TABLE_F64 = build_sigmoid_table(np.float64)
 
 import os
 
-# Row stride policy for float32 models: pad rows to a multiple of 32 floats (128 bytes) when
-# that costs at most LD_LINE_WASTE of the model, so that every row starts on a 128-byte line
-# and a warp-wide gather / RED.128 covers whole lines (d = 300 -> ld = 320: 4 + 4 + 2 L2
-# requests per row instead of 5 + 5 + 2..3; +7% words/s on the 1M-word model).  The kernels
-# only touch the dim columns that hold data; the pad stays zero.
+# Row stride policy: rows are a whole number of 32-byte sectors (a 16-byte cp.async whose
+# shared-memory destination and global source sit at different offsets within a sector
+# fetches one sector per lane instead of per pair of lanes, tools/probes/ldgsts_probe.cu),
+# and for float32 a whole number of 128-byte lines when that costs at most LD_LINE_WASTE of
+# the model, so that a warp-wide gather / RED.128 covers whole lines (d = 300 -> ld = 320:
+# 4 + 4 + 2 L2 requests per row instead of 5 + 5 + 2..3; +7% words/s on the 1M-word model).
+# The production kernel only touches the dim columns that hold data; the pad stays zero.
 LD_LINE_WASTE = float(os.environ.get("SGNS_LD_LINE_WASTE", "0.125"))
 
 
 def padded_ld(dim: int, dtype) -> int:
-    """Row stride in elements: a whole number of 16-byte chunks, line-aligned when cheap."""
-    per16 = 16 // np.dtype(dtype).itemsize
-    ld = -(-dim // per16) * per16
+    """Row stride in elements: whole 32-byte sectors, whole 128-byte lines when cheap."""
+    per32 = 32 // np.dtype(dtype).itemsize
+    ld = -(-dim // per32) * per32
     if np.dtype(dtype) == np.float32:
         line = -(-dim // 32) * 32
         if (line - dim) / dim <= LD_LINE_WASTE:
