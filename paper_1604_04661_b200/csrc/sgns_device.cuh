@@ -217,9 +217,21 @@ template <typename T> struct ModelView {
   T *out_dst;
   const T *in_src;
   const T *out_src;
-  int64_t ld;  // row stride in elements
-  int nvec;    // 16-byte chunks per row
+  int64_t ld;  // row stride in HBM, in elements (>= dim; model.py padded_ld)
+  int nvec;    // 16-byte chunks of a row that hold data (dim rounded up)
+  int lds;     // row stride of staged rows in shared memory: nvec chunks rounded up to 32 bytes
 };
+// Staged rows are packed at the data width, but keep the 32-byte sector phase of the model
+// rows: a 16-byte cp.async whose shared destination and global source differ in their offset
+// within a sector fetches one sector per lane (tools/probes/ldgsts_probe.cu).
+template <typename T>
+__host__ __device__ inline ModelView<T> make_view(T *in_dst, T *out_dst, const T *in_src, const T *out_src,
+                                                  int64_t ld, int dim) {
+  constexpr int per16 = 16 / (int)sizeof(T);
+  const int nvec = (dim + per16 - 1) / per16;
+  const int lds = ((nvec + 1) & ~1) * per16;
+  return ModelView<T>{in_dst, out_dst, in_src, out_src, ld, nvec, lds};
+}
 
 // Per-cell error, as batch_core_naive computes it (kernel_batched.py:174-190):
 // label - sigma and alpha * err in float64, each rounded once to the model dtype.
@@ -279,7 +291,8 @@ __device__ __forceinline__ void window_update(const ModelView<T> &mv, const int 
                                               int lane) {
   using V = typename Vec<T>::type;
   constexpr int VN = Vec<T>::N;
-  const int64_t ld = mv.ld;
+  const int64_t ld = mv.ld;  // HBM stride
+  const int lds = mv.lds;    // staged rows
   const int nvec = mv.nvec;
   const int nrows = m + k1;
 
@@ -287,7 +300,7 @@ __device__ __forceinline__ void window_update(const ModelView<T> &mv, const int 
   for (int r = 0; r < nrows; ++r) {
     const int id = ids_s[r];
     const T *src = (r < m ? mv.in_src : mv.out_src) + (int64_t)id * ld;
-    T *dst = rows_s + (int64_t)r * ld;
+    T *dst = rows_s + r * lds;
 #pragma unroll
     for (int j = 0; j < NCH; ++j) {
       const int c = lane + 32 * j;
@@ -306,7 +319,7 @@ __device__ __forceinline__ void window_update(const ModelView<T> &mv, const int 
 #pragma unroll
       for (int j = 0; j < NCH; ++j) {
         const int ch = lane + 32 * j;
-        a[j] = ch < nvec ? *reinterpret_cast<const V *>(rows_s + (int64_t)i * ld + ch * VN)
+        a[j] = ch < nvec ? *reinterpret_cast<const V *>(rows_s + i * lds + ch * VN)
                          : vzero(T());
       }
       T p[NV];
@@ -318,7 +331,7 @@ __device__ __forceinline__ void window_update(const ModelView<T> &mv, const int 
           for (int j = 0; j < NCH; ++j) {
             const int ch = lane + 32 * j;
             if (ch < nvec)
-              acc += vdot(a[j], *reinterpret_cast<const V *>(rows_s + (int64_t)(m + k) * ld + ch * VN));
+              acc += vdot(a[j], *reinterpret_cast<const V *>(rows_s + (m + k) * lds + ch * VN));
           }
         }
         p[k] = acc;
@@ -344,7 +357,7 @@ __device__ __forceinline__ void window_update(const ModelView<T> &mv, const int 
         if (ch < nvec) {
           V d = vzero(T());
           for (int k = 0; k < k1; ++k)
-            vfma(d, er_s[i * k1 + k], *reinterpret_cast<const V *>(rows_s + (int64_t)(m + k) * ld + ch * VN));
+            vfma(d, er_s[i * k1 + k], *reinterpret_cast<const V *>(rows_s + (m + k) * lds + ch * VN));
           vscale(d, alpha);
           red_add(dst + ch * VN, d);
         }
@@ -360,7 +373,7 @@ __device__ __forceinline__ void window_update(const ModelView<T> &mv, const int 
 #pragma unroll
         for (int q = 0; q < KG; ++q) acc[q] = vzero(T());
         for (int i = 0; i < m; ++i) {
-          const V a = *reinterpret_cast<const V *>(rows_s + (int64_t)i * ld + ch * VN);
+          const V a = *reinterpret_cast<const V *>(rows_s + i * lds + ch * VN);
 #pragma unroll
           for (int q = 0; q < KG; ++q)
             if (k0 + q < k1) vfma(acc[q], e_s[i * k1 + k0 + q], a);
@@ -404,9 +417,9 @@ __device__ __forceinline__ float4 ld_cg_f4(const float *p) {
 //   f2_dc_io     dC_k = sum_i (alpha err_ik) A_i, input-outer, NS x K1R accumulators
 //   f2_dc        the same sum column-outer (windows of more than 12 inputs)
 template <int NS, int NCH> struct F2Shape {
-  int ld, nvec, nslot, lane;
+  int ld, nvec, nslot, lane;  // ld: stride of the staged rows
   __device__ F2Shape(const ModelView<float> &mv, int lane_)
-      : ld((int)mv.ld), nvec(mv.nvec), nslot(2 * mv.nvec), lane(lane_) {}
+      : ld(mv.lds), nvec(mv.nvec), nslot(2 * mv.nvec), lane(lane_) {}
   // slot j of this lane is always in range for j < NS - 1 (NS = ceil(nslot / 32))
   __device__ bool slot_ok(int j) const { return j < NS - 1 || lane + 32 * j < nslot; }
   __device__ bool chunk_ok(int j) const { return j < NCH - 1 || lane + 32 * j < nvec; }
@@ -711,20 +724,20 @@ __device__ __forceinline__ void window_update_f2s(const ModelView<float> &mv, co
                                                   float *rows_s, float *e_s, int lane,
                                                   HotSink<NS> &hot) {  // register sink only
   constexpr int KM = 16;
-  const int64_t ld = mv.ld;
+  const int ld = mv.lds;  // staged rows
   const int nvec = mv.nvec, nslot = nvec * 2;
   auto slot_ok = [&](int j) { return j < NS - 1 || lane + 32 * j < nslot; };
   auto chunk_ok = [&](int j) { return j < NCH - 1 || lane + 32 * j < nvec; };
   for (int r = 0; r < m + k1; ++r) {
     const float *src = (r < m ? mv.in_src : mv.out_src) + off_s[r];
-    float *dst = rows_s + (int64_t)r * ld;
+    float *dst = rows_s + r * ld;
 #pragma unroll
     for (int j = 0; j < NCH; ++j)
       if (chunk_ok(j)) cp_async16(dst + (lane + 32 * j) * 4, src + (lane + 32 * j) * 4);
   }
   cp_async_wait_all();
   __syncwarp();
-  const float *c_s = rows_s + (int64_t)m * ld;
+  const float *c_s = rows_s + m * ld;
   float *er_s = e_s + m * KM;  // raw errors after the scaled ones
   const float2 alpha2 = make_float2(alpha, alpha);
   for (int i = 0; i < m; i += 2) {
@@ -734,8 +747,8 @@ __device__ __forceinline__ void window_update_f2s(const ModelView<float> &mv, co
 #pragma unroll
     for (int j = 0; j < NS; ++j) {
       const int col = 2 * (lane + 32 * j);
-      a0[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col) : f2zero();
-      a1[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + (int64_t)i1 * ld + col) : f2zero();
+      a0[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + i * ld + col) : f2zero();
+      a1[j] = slot_ok(j) ? *reinterpret_cast<const float2 *>(rows_s + i1 * ld + col) : f2zero();
     }
     float pp[2 * KM];
 #pragma unroll
@@ -744,7 +757,7 @@ __device__ __forceinline__ void window_update_f2s(const ModelView<float> &mv, co
       if (k < k1) {
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
-          const float2 c = slot_ok(j) ? *reinterpret_cast<const float2 *>(c_s + (int64_t)k * ld + 2 * (lane + 32 * j))
+          const float2 c = slot_ok(j) ? *reinterpret_cast<const float2 *>(c_s + k * ld + 2 * (lane + 32 * j))
                                       : f2zero();
           s0 = __ffma2_rn(a0[j], c, s0);
           s1 = __ffma2_rn(a1[j], c, s1);
@@ -776,7 +789,7 @@ __device__ __forceinline__ void window_update_f2s(const ModelView<float> &mv, co
       const float e0 = er_s[i * KM + k], e1 = er_s[i1 * KM + k];
 #pragma unroll
       for (int j = 0; j < NS; ++j) {
-        const float2 c = slot_ok(j) ? *reinterpret_cast<const float2 *>(c_s + (int64_t)k * ld + 2 * (lane + 32 * j))
+        const float2 c = slot_ok(j) ? *reinterpret_cast<const float2 *>(c_s + k * ld + 2 * (lane + 32 * j))
                                     : f2zero();
         d0[j] = __ffma2_rn(make_float2(e0, e0), c, d0[j]);
         d1[j] = __ffma2_rn(make_float2(e1, e1), c, d1[j]);
@@ -808,7 +821,7 @@ __device__ __forceinline__ void window_update_f2s(const ModelView<float> &mv, co
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = f2zero();
       for (int i = 0; i < m; ++i) {
-        const float2 a = *reinterpret_cast<const float2 *>(rows_s + (int64_t)i * ld + col);
+        const float2 a = *reinterpret_cast<const float2 *>(rows_s + i * ld + col);
         const float4 e03 = *reinterpret_cast<const float4 *>(e_s + i * KM + k0);
         const float4 e47 = *reinterpret_cast<const float4 *>(e_s + i * KM + k0 + 4);
         const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};

@@ -63,7 +63,7 @@ struct FastArgs {
 // offset within a 32-byte sector makes L1 fetch one sector per LANE (32 per warp
 // instruction instead of 16; tools/probes/ldgsts_probe.cu), so staged rows keep the phase
 // of the 128-byte-aligned model rows.
-__host__ __device__ inline int fast_lds(int nvec) { return (4 * nvec + 7) & ~7; }
+__host__ __device__ inline int fast_lds(int nvec) { return ((nvec + 1) & ~1) * 4; }  // = ModelView::lds
 
 struct FastSlab {
   int64_t rows, e, ids, roff, kept, koff, bw, cnt, cand, total;

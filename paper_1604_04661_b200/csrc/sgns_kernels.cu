@@ -49,8 +49,9 @@ struct Slab {
 // MODE_F2S: float32 8 < k1 <= 16, all rows staged; MODE_F2G: the same k1 in two register groups
 enum { MODE_SMEM = 0, MODE_F2 = 1, MODE_F2S = 2, MODE_F2G = 3 };
 // hot_rows: shared-memory hot-row sink rows of update_windows (H_in + H_out rows, see HotSink)
+// ld: stride of the staged rows (ModelView::lds); hot_ld: of the hot-row sinks (the HBM stride)
 __host__ __device__ inline Slab slab_layout(int mode, int64_t elem, int64_t ld, int mcap, int k1,
-                                            int kept_cap, int hot_rows = 0) {
+                                            int kept_cap, int hot_rows = 0, int64_t hot_ld = 0) {
   Slab s;
   s.rows = 0;
   const bool a_only = mode == MODE_F2 || mode == MODE_F2G;  // only the input rows are staged
@@ -63,7 +64,7 @@ __host__ __device__ inline Slab slab_layout(int mode, int64_t elem, int64_t ld, 
   s.kept = s.roff + round32((int64_t)(mcap + k1) * 4);
   s.off = s.kept + round32((int64_t)kept_cap * 4);
   s.hot = s.off + round32((int64_t)kept_cap * 4);
-  s.total = s.hot + round32((int64_t)hot_rows * ld * elem);
+  s.total = s.hot + round32((int64_t)hot_rows * hot_ld * elem);
   return s;
 }
 __host__ __device__ inline int64_t table_bytes(int64_t elem) { return round32(kSigBins * elem); }
@@ -154,7 +155,7 @@ __global__ void __maxnreg__((UpdRegs<MODE, NS, K1R>::v)) update_windows_kernel(U
   T *sig_s = reinterpret_cast<T *>(smem);
   load_table(sig_s, p.sig);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Slab L = slab_layout(MODE, sizeof(T), p.mv.ld, p.mcap, p.k1, 0, HOT ? p.hot_in + p.hot_out : 0);
+  const Slab L = slab_layout(MODE, sizeof(T), p.mv.lds, p.mcap, p.k1, 0, HOT ? p.hot_in + p.hot_out : 0, p.mv.ld);
   unsigned char *base = smem + table_bytes(sizeof(T)) + (int64_t)warp * L.total;
   T *rows_s = reinterpret_cast<T *>(base + L.rows);
   T *e_s = reinterpret_cast<T *>(base + L.e);
@@ -287,7 +288,7 @@ __global__ void __maxnreg__((UpdRegs<MODE, NS, K1R>::v)) drive_kernel(DriveArgs<
   if (wid >= p.n_workers) return;
   const int k1 = p.k_neg + 1;
   const int mcap = min(p.cap, 2 * p.window);
-  const Slab L = slab_layout(MODE, sizeof(T), p.mv.ld, mcap, k1, p.kept_cap);
+  const Slab L = slab_layout(MODE, sizeof(T), p.mv.lds, mcap, k1, p.kept_cap);
   unsigned char *base = smem + table_bytes(sizeof(T)) + (int64_t)warp * L.total;
   T *rows_s = reinterpret_cast<T *>(base + L.rows);
   T *e_s = reinterpret_cast<T *>(base + L.e);
@@ -649,7 +650,7 @@ static bool snapshot_mode(const ModelView<float> &mv) {
 template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT = false>
 static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
   auto kern = update_windows_kernel<T, MODE, NS, NCH, K1R, HOT>;
-  Slab L = slab_layout(MODE, sizeof(T), a.mv.ld, a.mcap, a.k1, 0);
+  Slab L = slab_layout(MODE, sizeof(T), a.mv.lds, a.mcap, a.k1, 0);
   int wpb = 0, bps = 0;
   int rc = choose_wpb(kern, table_bytes(sizeof(T)), L.total, &wpb, &bps);
   if (rc) return rc;
@@ -659,7 +660,7 @@ static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
     // both matrices (H <= 8), else M_out's row 0 beside the register sink for M_in's row 0
     const int cand[5][2] = {{8, 8}, {4, 4}, {2, 2}, {1, 1}, {0, 1}};
     for (const auto &hc : cand) {
-      const Slab Lh = slab_layout(MODE, sizeof(T), a.mv.ld, a.mcap, a.k1, 0, hc[0] + hc[1]);
+      const Slab Lh = slab_layout(MODE, sizeof(T), a.mv.lds, a.mcap, a.k1, 0, hc[0] + hc[1], a.mv.ld);
       int wh = 0, bh = 0;
       if (choose_wpb(kern, table_bytes(sizeof(T)), Lh.total, &wh, &bh) == 0 && wh * bh >= wpb * bps) {
         a.hot_in = hc[0];
@@ -687,7 +688,7 @@ template <typename T, int MODE, int NS, int NCH, int K1R, int RNG>
 static int launch_drive_t(DriveArgs<T> a, int wpb_req, cudaStream_t st, int *resident = nullptr) {
   auto kern = drive_kernel<T, MODE, NS, NCH, K1R, RNG>;
   const int k1 = a.k_neg + 1;
-  const Slab L = slab_layout(MODE, sizeof(T), a.mv.ld, std::min(a.cap, 2 * a.window), k1, a.kept_cap);
+  const Slab L = slab_layout(MODE, sizeof(T), a.mv.lds, std::min(a.cap, 2 * a.window), k1, a.kept_cap);
   int wpb = 0, bps = 0;
   int rc = choose_wpb(kern, table_bytes(sizeof(T)), L.total, &wpb, &bps);
   if (rc) return rc;
@@ -719,8 +720,8 @@ static int drive_f2s(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
   const int k1 = a.k_neg + 1, mcap = std::min(a.cap, 2 * a.window);
   if (prefer_staged(drive_kernel<float, MODE_F2S, NS, NCH, 16, RNG>,
                     drive_kernel<float, MODE_F2G, NS, NCH, 8, RNG>,
-                    slab_layout(MODE_F2S, 4, a.mv.ld, mcap, k1, a.kept_cap).total,
-                    slab_layout(MODE_F2G, 4, a.mv.ld, mcap, k1, a.kept_cap).total))
+                    slab_layout(MODE_F2S, 4, a.mv.lds, mcap, k1, a.kept_cap).total,
+                    slab_layout(MODE_F2G, 4, a.mv.lds, mcap, k1, a.kept_cap).total))
     return launch_drive_t<float, MODE_F2S, NS, NCH, 16, RNG>(a, wpb, st, res);
   // F2G's K1R: rows of its second output group
   if (k1 <= 12) return launch_drive_t<float, MODE_F2G, NS, NCH, 4, RNG>(a, wpb, st, res);
@@ -729,7 +730,7 @@ static int drive_f2s(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
 
 template <int RNG>
 static int drive_f32(DriveArgs<float> a, int wpb, cudaStream_t st, int *res) {
-  const int ns = ns_for(a.mv.ld);
+  const int ns = ns_for(4 * a.mv.nvec);
   if (a.k_neg + 1 > 8 && a.k_neg + 1 <= 16 && offsets32_ok(a.vocab, a.mv.ld)) {
     switch (ns) {
       case 1: return drive_f2s<1, RNG>(a, wpb, st, res);
@@ -797,8 +798,8 @@ static int update_f2s(UpdateArgs<float> a, cudaStream_t st) {
   const char *force = std::getenv("SGNS_UPDATE_BODY");  // experiments: "g" / "s" force F2G / F2S
   const bool staged = force ? force[0] == 's' : prefer_staged(update_windows_kernel<float, MODE_F2S, NS, NCH, 16, false>,
                                     update_windows_kernel<float, MODE_F2G, NS, NCH, 8, false>,
-                                    slab_layout(MODE_F2S, 4, a.mv.ld, a.mcap, a.k1, 0).total,
-                                    slab_layout(MODE_F2G, 4, a.mv.ld, a.mcap, a.k1, 0).total);
+                                    slab_layout(MODE_F2S, 4, a.mv.lds, a.mcap, a.k1, 0).total,
+                                    slab_layout(MODE_F2G, 4, a.mv.lds, a.mcap, a.k1, 0).total);
   if (staged)
     return hot ? launch_update_t<float, MODE_F2S, NS, NCH, 16, true>(a, st)
                : launch_update_t<float, MODE_F2S, NS, NCH, 16, false>(a, st);
@@ -811,7 +812,7 @@ static int update_f2s(UpdateArgs<float> a, cudaStream_t st) {
 }
 
 int update_f32(UpdateArgs<float> a, cudaStream_t st) {
-  const int ns = ns_for(a.mv.ld);
+  const int ns = ns_for(4 * a.mv.nvec);
   if (a.k1 > 8 && a.k1 <= 16 && offsets32_ok(a.vocab, a.mv.ld)) {
     switch (ns) {
       case 1: return update_f2s<1>(a, st);
@@ -864,7 +865,7 @@ template <typename T>
 static void fill_drive_args(DriveArgs<T> &a, const sgns_drive_params *p) {
   std::memset(&a, 0, sizeof(a));
   T *mi = static_cast<T *>(p->d_m_in), *mo = static_cast<T *>(p->d_m_out);
-  a.mv = ModelView<T>{mi, mo, mi, mo, p->ld, (int)(p->ld * (int64_t)sizeof(T) / 16)};
+  a.mv = make_view<T>(mi, mo, mi, mo, p->ld, p->dim);
   a.ids = p->d_ids;
   a.offsets = p->d_offsets;
   a.keep = p->d_keep_probs;
@@ -971,7 +972,7 @@ int fast_dispatch(const sgns_drive_params *p, cudaStream_t st, int *resident) {
   FastArgs a;
   std::memset(&a, 0, sizeof(a));
   float *mi = static_cast<float *>(p->d_m_in), *mo = static_cast<float *>(p->d_m_out);
-  a.mv = ModelView<float>{mi, mo, mi, mo, p->ld, (p->dim + 3) / 4};  // nvec: the columns that hold data
+  a.mv = make_view<float>(mi, mo, mi, mo, p->ld, p->dim);
   a.ids = p->d_ids;
   a.offsets = p->d_offsets;
   a.keep = p->d_keep_probs;
@@ -1195,9 +1196,9 @@ int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, cons
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (dtype == SGNS_F32) {
     UpdateArgs<float> a;
-    a.mv = ModelView<float>{static_cast<float *>(d_m_in_dst), static_cast<float *>(d_m_out_dst),
+    a.mv = make_view<float>(static_cast<float *>(d_m_in_dst), static_cast<float *>(d_m_out_dst),
                             static_cast<const float *>(d_m_in_src), static_cast<const float *>(d_m_out_src),
-                            ld, (int)(ld / 4)};
+                            ld, dim);
     a.in_off = d_in_off; a.in_ids = d_in_ids; a.out_ids = d_out_ids;
     a.n_win = n_windows; a.k1 = k1; a.mcap = max_inputs; a.vocab = vocab;
     a.alpha = static_cast<const float *>(d_alpha);
@@ -1210,9 +1211,9 @@ int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, cons
   }
   if (dtype == SGNS_F64) {
     UpdateArgs<double> a;
-    a.mv = ModelView<double>{static_cast<double *>(d_m_in_dst), static_cast<double *>(d_m_out_dst),
+    a.mv = make_view<double>(static_cast<double *>(d_m_in_dst), static_cast<double *>(d_m_out_dst),
                              static_cast<const double *>(d_m_in_src),
-                             static_cast<const double *>(d_m_out_src), ld, (int)(ld / 2)};
+                             static_cast<const double *>(d_m_out_src), ld, dim);
     a.in_off = d_in_off; a.in_ids = d_in_ids; a.out_ids = d_out_ids;
     a.n_win = n_windows; a.k1 = k1; a.mcap = max_inputs; a.vocab = vocab;
     a.alpha = static_cast<const double *>(d_alpha);
