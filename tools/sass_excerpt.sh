@@ -12,7 +12,7 @@ echo "## opcode histogram (static instruction count)"
 grep -oE "^\s+/\*[0-9a-f]+\*/\s+(@!?U?P[0-9T] )?[A-Z0-9_]+" $T | awk '{print $NF}' | sort | uniq -c | sort -rn | head -30
 echo "## packed FP32, async copies, vector reductions (full forms)"
 grep -oE "(FFMA2|FMUL2|FADD2|LDGSTS|REDG|LDG)[A-Za-z0-9_.]*" $T | sort | uniq -c
-echo "## dC pass inner loop (column-outer over the staged rows: LDS.64 row slot, LDS.128 x2 errors, 6 FFMA2)"
+echo "## dC pass inner loop (input-outer: one staged row = LDS.128 x2 + LDS.64, its error row = LDS.128 + LDS.64, 30 FFMA2 with the error as broadcast .F32 operand)"
 L=$(grep -n "LDS.128" $T | tail -4 | head -1 | cut -d: -f1)
 sed -n "$((L-24)),$((L+48))p" $T | grep -v '^\s*/\* 0x' | sed 's@ */\* 0x[0-9a-f]* \*/@@' | grep -v '^\s*$'
 rm -f $T
