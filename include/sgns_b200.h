@@ -60,7 +60,14 @@ typedef struct sgns_worker {
   int64_t inputs;                     /* sum of chunk input counts (roofline accounting) */
 } sgns_worker;
 
-/* One batch of packed windows (the CSR form of a list of Minibatch,
+/* Row stride ld (elements) of M_in / M_out: any multiple of 16 bytes >= dim.  The kernels
+ * read and write the dim data columns only (whole 16-byte chunks: columns from dim up to the
+ * next multiple of 16 bytes must be zero, as sgns_init_model leaves them); the rest of a
+ * padded row is never touched.  Fastest when rows start on 128-byte lines (float32: ld a
+ * multiple of 32, e.g. 320 at dim = 300; the Python package's padded_ld allocates that way),
+ * and at least on 32-byte sectors (ld * sizeof(elem) % 32 == 0): see DESIGN.md section 2.
+ *
+ * One batch of packed windows (the CSR form of a list of Minibatch,
  * kernel_batched.py:37-54): window w has inputs in_ids[in_off[w]:in_off[w+1]]
  * and outputs out_ids[w*k1 : (w+1)*k1], target first.  n_windows == 0 is a no-op
  * (SGNS_OK before any pointer is inspected). */

@@ -13,9 +13,8 @@ and the GPU model after the sentence must equal it at
     |gpu - oracle| <= 1e-5 |oracle| + 1e-7          (tests/test_acceptance.py:199-209)
 
 on every entry.  The vocabulary is tiny (12 ids), so consecutive windows of a sentence
-share their target and negative rows all the time: the kernel's u -> u+1 output-row
-prefetch and its collision patch (sgns_fast.cuh:494-504) are exercised on most windows
-(the test counts them).  batch_cap = 4 splits positions into chunks that share the
+share their target and negative rows all the time: window u + 1's output rows, loaded
+right after u's scatters, must read them (the test counts such windows).  batch_cap = 4 splits positions into chunks that share the
 target.  A sentence whose replay meets a score within the float32 rounding distance
 of a sigma-bin edge (oracle/pin.py near_edge) may
 legally differ (SURVEY 8c bin-flip protocol): it is counted and skipped, and both sides
@@ -66,16 +65,29 @@ CASES += [(300, k, 16) for k in (8, 9, 10, 12, 14, 15)] + [(100, 10, 16), (512, 
                                                           (320, 15, 16), (300, 15, 4), (64, 9, 4)]
 
 
-def _pin_case(D, k, cap, window=5, V=12, n_sent=60, lo=4, hi=12, seed_extra=0):
+def _device_model(m_in, m_out, ld=None):
+    """The package's own row stride (model.py padded_ld), or an explicit one."""
     import paper_1604_04661_b200 as P
-    from paper_1604_04661_b200.model import DeviceModel, SIGMOID_TABLE_F32
+    from paper_1604_04661_b200.model import DeviceModel
+    if ld is None:
+        return DeviceModel.from_host(P.EmbeddingModel(m_in, m_out))
+    V, D = m_in.shape
+    st = torch.zeros((2, V, ld), dtype=torch.float32, device="cuda")
+    st[0, :, :D].copy_(torch.from_numpy(m_in))
+    st[1, :, :D].copy_(torch.from_numpy(m_out))
+    return DeviceModel(st[0], st[1], D, st)
+
+
+def _pin_case(D, k, cap, window=5, V=12, n_sent=60, lo=4, hi=12, seed_extra=0, ld=None):
+    import paper_1604_04661_b200 as P
+    from paper_1604_04661_b200.model import SIGMOID_TABLE_F32
     from oracle import pin
     rng = np.random.default_rng(1000 * D + 10 * k + cap + 7919 * window + seed_extra)
     ids, off, counts = pin.tiny_corpus(rng, V, n_sent, lo, hi)
     scale = 0.6 * D ** -0.25  # scores ~ N(0, 0.36): most cells inside the table's [-6, 6)
     m_in = (rng.normal(size=(V, D)) * scale).astype(np.float32)
     m_out = (rng.normal(size=(V, D)) * scale).astype(np.float32)
-    dm = DeviceModel.from_host(P.EmbeddingModel(m_in, m_out))
+    dm = _device_model(m_in, m_out, ld)
     run = _fast_run(ids, off, counts, dm, k=k, cap=cap, window=window)
     t = pin.replay_sentences(run, dm, n_sent, cap, k + 1, SIGMOID_TABLE_F32)
     assert run.done
@@ -87,6 +99,21 @@ def test_fast_kernel_per_sentence_vs_oracle(D, k, cap):
     t = _pin_case(D, k, cap)
     assert t["windows"] > 200 and t["shared_next"] > t["windows"] // 2, t
     assert t["compared"] >= 0.7 * 60, t  # the rest hold a score at a sigma-bin edge
+    assert t["loss_worst"] <= 1.0, t
+    assert t["worst"] <= 1.0, t
+
+
+# Row strides other than the package's line-aligned default (the C ABI takes any stride that
+# is a multiple of 16 bytes): dim rounded to 16 bytes only (rows out of sector phase), to a
+# 32-byte sector, and a generous pad; the kernels touch the dim data columns only.
+LDCASES = [(300, 5, 16, 300), (300, 5, 16, 304), (300, 5, 16, 384), (300, 10, 16, 300), (100, 5, 16, 100),
+           (100, 15, 16, 104), (30, 5, 4, 32), (130, 7, 16, 132)]
+
+
+@pytest.mark.parametrize("D,k,cap,ld", LDCASES, ids=[f"d{d}_k{k}_cap{c}_ld{l}" for d, k, c, l in LDCASES])
+def test_fast_kernel_row_strides(D, k, cap, ld):
+    t = _pin_case(D, k, cap, ld=ld)
+    assert t["windows"] > 200 and t["compared"] >= 0.7 * 60, t
     assert t["loss_worst"] <= 1.0, t
     assert t["worst"] <= 1.0, t
 

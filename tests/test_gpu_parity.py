@@ -186,6 +186,20 @@ def _random_windows(rng, V, n, m_max, k, disjoint=False):
                                        ("f64", 24, 3)])
 def test_disjoint_windows_equal_sequential(dtype, D, k):
     """P2: a batch of row-disjoint windows == the sequential oracle application."""
+    _p2_disjoint(dtype, D, k)
+
+
+@pytest.mark.parametrize("dtype,D,k,ld", [("f32", 300, 5, 300), ("f32", 300, 5, 304), ("f32", 300, 15, 300),
+                                          ("f32", 100, 12, 100), ("f32", 200, 10, 256), ("f64", 30, 3, 30),
+                                          ("f64", 300, 5, 302)])
+def test_disjoint_windows_any_row_stride(dtype, D, k, ld):
+    """P2 on models whose row stride is not the package's own (model.py padded_ld): the C
+    ABI takes any stride that is a multiple of 16 bytes; only the dim data columns are
+    touched, staged rows are packed at the data width."""
+    _p2_disjoint(dtype, D, k, ld)
+
+
+def _p2_disjoint(dtype, D, k, ld=None):
     P, O = _pkg(), _oracle()
     from paper_1604_04661_b200.kernel_batched import DeviceWindowBatch, WindowBatch
     from paper_1604_04661_b200.model import DeviceModel, SIGMOID_TABLE_F32, SIGMOID_TABLE_F64
@@ -198,9 +212,17 @@ def test_disjoint_windows_equal_sequential(dtype, D, k):
     wins = _random_windows(rng, V, 150, 10, k, disjoint=True)
     alpha = 0.025
     wb = WindowBatch.from_minibatches([P.Minibatch(a, b) for a, b in wins])
-    dm = DeviceModel.from_host(base)
+    if ld is None:
+        dm = DeviceModel.from_host(base)
+    else:
+        st = torch.full((2, V, ld), 7.0, dtype=torch.float64 if dtype == "f64" else torch.float32, device="cuda")
+        st[0, :, :D].copy_(torch.from_numpy(base.input_vectors))
+        st[1, :, :D].copy_(torch.from_numpy(base.output_vectors))
+        dm = DeviceModel(st[0], st[1], D, st)
     P.update_windows(dm, DeviceWindowBatch(wb), alpha)
     got = dm.to_host()
+    if ld is not None and ld > D:  # the pad columns are never written
+        assert bool((dm.storage[:, :, D:] == 7.0).all())
     ref_in, ref_out = base.input_vectors.copy(), base.output_vectors.copy()
     tab = SIGMOID_TABLE_F64 if dtype == "f64" else SIGMOID_TABLE_F32
     flips = 0

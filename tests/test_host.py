@@ -154,3 +154,15 @@ def test_sampler_rejects_tables_without_a_second_word():
         DeviceSampler(np.array([7, 0, 0]), "philox", device="cpu")
     with pytest.raises(ValueError):
         DeviceSampler(np.array([5, 0]), "splitmix", table_length=10, device="cpu")
+
+
+def test_row_stride_policy():
+    """model.py padded_ld: whole 32-byte sectors; float32 rows on whole 128-byte lines when
+    that costs at most 12.5% (DESIGN 2)."""
+    from paper_1604_04661_b200.model import padded_ld
+    f32 = {300: 320, 200: 224, 100: 104, 128: 128, 4: 8, 7: 8, 64: 64, 512: 512, 500: 512, 33: 40, 29: 32}
+    for dim, ld in f32.items():
+        assert padded_ld(dim, np.float32) == ld, (dim, padded_ld(dim, np.float32))
+        assert ld >= dim and ld % 8 == 0
+    for dim, ld in {300: 300, 5: 8, 101: 104}.items():
+        assert padded_ld(dim, np.float64) == ld
