@@ -65,6 +65,9 @@ CASES += [(300, k, 16) for k in (8, 9, 10, 12, 14, 15)] + [(100, 10, 16), (512, 
                                                           (320, 15, 16), (300, 15, 4), (64, 9, 4)]
 
 
+PAD_SENTINEL = 7.0
+
+
 def _device_model(m_in, m_out, ld=None):
     """The package's own row stride (model.py padded_ld), or an explicit one."""
     import paper_1604_04661_b200 as P
@@ -73,6 +76,7 @@ def _device_model(m_in, m_out, ld=None):
         return DeviceModel.from_host(P.EmbeddingModel(m_in, m_out))
     V, D = m_in.shape
     st = torch.zeros((2, V, ld), dtype=torch.float32, device="cuda")
+    st[:, :, -(-D // 4) * 4:] = PAD_SENTINEL  # beyond the last 16-byte data chunk: never touched
     st[0, :, :D].copy_(torch.from_numpy(m_in))
     st[1, :, :D].copy_(torch.from_numpy(m_out))
     return DeviceModel(st[0], st[1], D, st)
@@ -91,6 +95,8 @@ def _pin_case(D, k, cap, window=5, V=12, n_sent=60, lo=4, hi=12, seed_extra=0, l
     run = _fast_run(ids, off, counts, dm, k=k, cap=cap, window=window)
     t = pin.replay_sentences(run, dm, n_sent, cap, k + 1, SIGMOID_TABLE_F32)
     assert run.done
+    if ld is not None and ld > -(-D // 4) * 4:
+        assert bool((dm.storage[:, :, -(-D // 4) * 4:] == PAD_SENTINEL).all()), "pad columns were written"
     return t
 
 
