@@ -221,7 +221,10 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
   const int mcap = min(p.cap, 2 * p.window);
   const FastSlab L = fast_slab(fast_lds(p.mv.nvec), mcap, K1T, p.kept_cap);
   unsigned char *base = smem + round16_(kSigBins * 4) + (int64_t)warp * L.total;
-  float *rows_s = reinterpret_cast<float *>(base + L.rows);
+  // PAIR: ONE staged copy of the window's input rows per pair, in the leader's slab; each
+  // warp gathers every other row (the pair barriers below order it against both readers)
+  float *rows_s = reinterpret_cast<float *>(
+      (PAIR ? smem + round16_(kSigBins * 4) + (int64_t)(warp & ~1) * L.total : base) + L.rows);
   float *e_s = reinterpret_cast<float *>(base + L.e);
   int *ids_b = reinterpret_cast<int *>(base + L.ids);
   uint32_t *roff_b = reinterpret_cast<uint32_t *>(base + L.roff);
@@ -454,7 +457,7 @@ __global__ void __maxnreg__((FastRegs<NS, K1R>::v)) drive_fast_kernel(FastArgs p
       uint32_t *off_n = roff_b + (cur ^ 1) * idsn;
       const int m = u.mc;
       // A rows of u -> smem
-      for (int r = 0; r < m; ++r) {
+      for (int r = PAIR ? (warp & 1) : 0; r < m; r += PAIR ? 2 : 1) {
         const float *src = in_src_l + off_s[r];
         float *dst = rows_s + r * ld + 4 * lane;
 #pragma unroll
