@@ -35,6 +35,8 @@ sys.path.insert(0, ROOT)
 METRIC = "training words/sec at 1/2/4/8 B200 and achieved HBM GB/s vs peak (d=300,w=5,K=5)"
 UNIT = "words/s"
 DIM, WINDOW, NEG, SUBSAMPLE, ALPHA0 = 300, 5, 5, 1e-4, 0.025
+# diagnostic only (kernel experiments at other row widths); the headline is d = 300
+DIM = int(os.environ.get("SGNS_BENCH_DIM", DIM))
 
 
 def parse():
@@ -53,6 +55,9 @@ def parse():
                     help="--config micro: id distribution (uniform = no hot rows, diagnostic)")
     ap.add_argument("--micro-shape", default="",
                     help="--config micro: run only shapes matching 'n_win,d,w,K[,dyn]' (e.g. 65536,300,5,5), ';'-separated, in that order")
+    ap.add_argument("--micro-grid", action="store_true",
+                    help="--config micro: the whole configs[1] grid d in {100,200,300} x w in {2,5,10} x "
+                         "K in {5,10,15} at 65,536 windows (27 shapes) instead of the default selection")
     ap.add_argument("--micro-no-flush", action="store_true",
                     help="--config micro diagnostic: no L2 flush between launches (not the configs[1] protocol)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -106,16 +111,20 @@ h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
 bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
         nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
 out = open(sys.argv[2], "w", buffering=1)
-print("ready", flush=True)
+mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+n = 0
 while True:
     try:
-        t = time.time()
         sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
         r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        t = time.time()  # stamped when the values are in hand (a cold first query can take > 100 ms)
         out.write("%.6f %d %d %s\n" % (t, sm, mx, ",".join(str(int(bool(r & b))) for b in bits)))
+        n += 1
+        if n == 3:  # the queries are warm: the parent may start its steps
+            print("ready", flush=True)
     except Exception:
-        pass
+        if n < 3:
+            sys.exit(1)  # NVML cannot be queried: the parent falls back to nvidia-smi
     time.sleep(0.002)
 """
 
@@ -180,10 +189,17 @@ while True:
                         continue
             os.unlink(self.path + ".smi")
         inside = [x for x in samples if self.t0 is None or self.t0 <= x[0] <= (self.t1 or x[0])]
+        window = "timed region"
+        if not inside and samples and self.t0 is not None:
+            # no query returned inside the region (a stalled NVML call): report the samples
+            # bracketing it rather than nothing, and say so
+            before = [x for x in samples if x[0] < self.t0][-2:]
+            after = [x for x in samples if x[0] > (self.t1 or self.t0)][:2]
+            inside, window = before + after, "bracketing samples (none inside the timed region)"
         reasons = sorted({n for x in inside for n, on in zip(self.NAMES, x[3]) if on})
         return {"sm_mhz": float(np.median([x[1] for x in inside])) if inside else None,
                 "sm_max_mhz": float(max(x[2] for x in inside)) if inside else None,
-                "samples": len(inside), "source": self.source, "reasons": reasons}
+                "samples": len(inside), "window": window, "source": self.source, "reasons": reasons}
 
 
 def build_corpus(args, device):
@@ -331,6 +347,8 @@ def micro_bench(args):
               (65536, 100, 5, 5, False), (65536, 200, 5, 5, False), (65536, 300, 2, 5, False),
               (65536, 300, 10, 5, False), (65536, 300, 5, 10, False), (65536, 300, 5, 15, False),
               (65536, 100, 10, 15, False), (65536, 300, 5, 5, True)]
+    if args.micro_grid:
+        shapes = [(65536, d, w, k, False) for d in (100, 200, 300) for w in (2, 5, 10) for k in (5, 10, 15)]
     T = len(os.sched_getaffinity(0))
     ranks = np.arange(1, V + 1, dtype=np.float64)
     pz = 1.0 / ranks if args.micro_ids == "zipf" else np.ones_like(ranks)

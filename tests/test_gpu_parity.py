@@ -161,12 +161,12 @@ def test_init_model_bitwise():
         assert not m32.output_vectors.any()
 
 
-def _random_windows(rng, V, n, m_max, k, disjoint=False):
+def _random_windows(rng, V, n, m_max, k, disjoint=False, m_fixed=None):
     wins = []
     pool = rng.permutation(V)
     used = 0
     for _ in range(n):
-        m = int(rng.integers(1, m_max + 1))
+        m = int(rng.integers(1, m_max + 1)) if m_fixed is None else m_fixed
         if disjoint:
             ids = pool[used:used + m + k + 1]
             used += m + k + 1
@@ -255,15 +255,28 @@ def test_snapshot_conflicting_windows(dtype, D, k, body, monkeypatch):
     Zipf(1.3) puts id 0 in ~30% of the slots here."""
     if body:
         monkeypatch.setenv("SGNS_UPDATE_BODY", body)
+    _p3_snapshot(dtype, D, k)
+
+
+@pytest.mark.parametrize("D", [100, 200, 300])
+@pytest.mark.parametrize("w", [2, 5, 10])
+@pytest.mark.parametrize("k", [5, 10, 15])
+def test_snapshot_configs1_grid(D, w, k):
+    """P3 on every shape of BASELINE.json configs[1] (d x w x K, full windows m = 2w as the
+    microbench runs them: `bench.py --config micro --micro-grid`), Zipf-conflicting rows."""
+    _p3_snapshot("f32", D, k, m_fixed=2 * w, n_win=300)
+
+
+def _p3_snapshot(dtype, D, k, m_fixed=None, n_win=400):
     P, O = _pkg(), _oracle()
     from paper_1604_04661_b200.kernel_batched import DeviceWindowBatch, WindowBatch
     from paper_1604_04661_b200.model import DeviceModel, SIGMOID_TABLE_F32, SIGMOID_TABLE_F64
-    rng = np.random.default_rng(7 + D + k)
+    rng = np.random.default_rng(7 + D + k + (0 if m_fixed is None else 1000 * m_fixed))
     npdt = np.float64 if dtype == "f64" else np.float32
     V = 500
     base = P.EmbeddingModel((rng.normal(size=(V, D)) * D ** -0.25).astype(npdt),
                             (rng.normal(size=(V, D)) * D ** -0.25).astype(npdt))
-    wins = _random_windows(rng, V, 400, 10, k)
+    wins = _random_windows(rng, V, n_win, 10, k, m_fixed=m_fixed)
     wb = WindowBatch.from_minibatches([P.Minibatch(a, b) for a, b in wins])
     alphas = rng.uniform(0.001, 0.03, size=len(wins))
     src = DeviceModel.from_host(base)
