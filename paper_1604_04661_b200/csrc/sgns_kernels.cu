@@ -796,10 +796,11 @@ static int update_f2s(UpdateArgs<float> a, cudaStream_t st) {
   constexpr int NCH = (NS + 1) / 2;
   const bool hot = snapshot_mode(a.mv);
   const char *force = std::getenv("SGNS_UPDATE_BODY");  // experiments: "g" / "s" force F2G / F2S
-  const bool staged = force ? force[0] == 's' : prefer_staged(update_windows_kernel<float, MODE_F2S, NS, NCH, 16, false>,
-                                    update_windows_kernel<float, MODE_F2G, NS, NCH, 8, false>,
-                                    slab_layout(MODE_F2S, 4, a.mv.lds, a.mcap, a.k1, 0).total,
-                                    slab_layout(MODE_F2G, 4, a.mv.lds, a.mcap, a.k1, 0).total);
+  // The two-group body is never slower than the all-staged one on the configs[1] grid
+  // (18 shapes with K = 10 / 15, profiles/round2_microbench_bodies_grid.jsonl: equal where
+  // both keep 16 warps per SM at d = 300, +4..12% at d = 100 / 200 with w <= 5, 1.3-1.9x
+  // where staging the output rows costs resident warps), so it is the choice; "s" forces F2S.
+  const bool staged = force && force[0] == 's';
   if (staged)
     return hot ? launch_update_t<float, MODE_F2S, NS, NCH, 16, true>(a, st)
                : launch_update_t<float, MODE_F2S, NS, NCH, 16, false>(a, st);
