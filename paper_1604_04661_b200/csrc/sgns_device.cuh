@@ -471,15 +471,29 @@ template <int NS> struct HotSink {
   uint32_t in_lim, out_lim;  // a row offset (id * ld) below the limit is hot
 };
 
-template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT>
+// an error row of NV floats (the first K1R needed) as 128-bit shared loads
+template <int NV, int K1R>
+__device__ __forceinline__ void load_errors(float (&ev)[NV], const float *ep) {
+#pragma unroll
+  for (int q = 0; q < NV / 4; ++q) {
+    if (4 * q < K1R || q < 2) {  // (the 8-float rows are always read whole, as before)
+      const float4 e = *reinterpret_cast<const float4 *>(ep + 4 * q);
+      ev[4 * q] = e.x; ev[4 * q + 1] = e.y; ev[4 * q + 2] = e.z; ev[4 * q + 3] = e.w;
+    } else {
+      ev[4 * q] = ev[4 * q + 1] = ev[4 * q + 2] = ev[4 * q + 3] = 0.f;
+    }
+  }
+}
+
+// NV: padded outputs per input in the reduction and the error rows (8; 16 for the wide body)
+template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT, int NV = 8>
 __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const ModelView<float> &mv,
                                             const F2Shape<NS, NCH> &sh, const uint32_t *off_s,
                                             int m, int k1, float alpha, bool exact,
                                             const float *sig_s, bool want_loss, double &loss_acc,
                                             long long &cell_acc, const float *rows_s, float *e_s,
                                             HotSink<NS> &hot, int kbase = 0) {
-  constexpr int NV = 8;
-  static_assert(K1R <= NV, "K1R <= 8");
+  static_assert(K1R <= NV && (NV == 8 || NV == 16), "K1R <= NV");
   const int lane = sh.lane;
   cp_async_wait_all();
   __syncwarp();  // staged rows were copied in 16-byte lanes, read in 8-byte lanes
@@ -510,13 +524,13 @@ __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const Mo
     }
     const float s = transpose_reduce<2 * NV>(pp, lane);
     const int v = reduced_index<2 * NV>(lane);
-    const int hk = v >> 3, kk = v & 7;
+    const int hk = v >> Log2<NV>::v, kk = v & (NV - 1);
     float er = 0.f, es = 0.f;
     if (kk < k1 && (hk == 0 || two)) {
       if (exact) cell_error<float>(s, kbase + kk, alpha, true, sig_s, er, es);
       else cell_error_f32(s, kbase + kk, alpha, sig_s, er, es);
-      if ((lane & 1) == 0) {
-        e_s[(i + hk) * 8 + kk] = es;
+      if ((lane & (16 / NV - 1)) == 0) {  // one lane per value (2 * NV values over 32 lanes)
+        e_s[(i + hk) * NV + kk] = es;
         if (want_loss) {
           loss_acc += softplus(kbase + kk == 0 ? -(double)s : (double)s);
           cell_acc += 1;
@@ -529,9 +543,8 @@ __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const Mo
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (h == 1 && !two) break;
-      const float4 e03 = *reinterpret_cast<const float4 *>(e_s + (i + h) * 8);
-      const float4 e47 = *reinterpret_cast<const float4 *>(e_s + (i + h) * 8 + 4);
-      const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
+      float ev[NV];
+      load_errors<NV, K1R>(ev, e_s + (i + h) * NV);
       float2 d[NS];
 #pragma unroll
       for (int k = 0; k < K1R; ++k) {
@@ -565,7 +578,7 @@ __device__ __forceinline__ void f2_score_da(const float2 (&c)[K1R][NS], const Mo
   __syncwarp();
 }
 
-template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT = false>
+template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT = false, int NV = 8>
 __device__ __forceinline__ void f2_dc(const ModelView<float> &mv, const F2Shape<NS, NCH> &sh,
                                       const uint32_t *off_s, int m, int k1, const float *rows_s,
                                       const float *e_s, HotSink<NS> *hot = nullptr) {
@@ -580,11 +593,10 @@ __device__ __forceinline__ void f2_dc(const ModelView<float> &mv, const F2Shape<
     for (int k = 0; k < K1R; ++k) acc[k] = f2zero();
     const float *ap = rows_s + col;
     const float *ep = e_s;
-    for (int i = 0; i < m; ++i, ap += sh.ld, ep += 8) {
+    for (int i = 0; i < m; ++i, ap += sh.ld, ep += NV) {
       const float2 a0 = *reinterpret_cast<const float2 *>(ap);
-      const float4 e03 = *reinterpret_cast<const float4 *>(ep);
-      const float4 e47 = *reinterpret_cast<const float4 *>(ep + 4);
-      const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
+      float ev[NV];
+      load_errors<NV, K1R>(ev, ep);
 #pragma unroll
       for (int k = 0; k < K1R; ++k)
         if (kk_ok(k)) acc[k] = __ffma2_rn(make_float2(ev[k], ev[k]), a0, acc[k]);
@@ -606,7 +618,7 @@ __device__ __forceinline__ void f2_dc(const ModelView<float> &mv, const F2Shape<
 
 // dC input-outer: NS x K1R float2 accumulators in registers (the caller's C registers
 // are dead by now), each staged row slot and error row read once
-template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT = false>
+template <int NS, int NCH, int K1R, bool EXACT_K, bool HOT = false, int NV = 8>
 __device__ __forceinline__ void f2_dc_io(const ModelView<float> &mv, const F2Shape<NS, NCH> &sh,
                                          const uint32_t *off_s, int m, int k1, const float *rows_s,
                                          const float *e_s, HotSink<NS> *hot = nullptr) {
@@ -619,10 +631,9 @@ __device__ __forceinline__ void f2_dc_io(const ModelView<float> &mv, const F2Sha
     for (int k = 0; k < K1R; ++k) acc[j][k] = f2zero();
   const float *ap = rows_s + 2 * sh.lane;
   const float *ep = e_s;
-  for (int i = 0; i < m; ++i, ap += sh.ld, ep += 8) {
-    const float4 e03 = *reinterpret_cast<const float4 *>(ep);
-    const float4 e47 = *reinterpret_cast<const float4 *>(ep + 4);
-    const float ev[8] = {e03.x, e03.y, e03.z, e03.w, e47.x, e47.y, e47.z, e47.w};
+  for (int i = 0; i < m; ++i, ap += sh.ld, ep += NV) {
+    float ev[NV];
+    load_errors<NV, K1R>(ev, ep);
 #pragma unroll
     for (int j = 0; j < NS; ++j) {
       const float2 a0 = sh.slot_ok(j) ? *reinterpret_cast<const float2 *>(ap + 64 * j) : f2zero();
@@ -670,6 +681,28 @@ __device__ __forceinline__ void window_update_f2(const ModelView<float> &mv, con
   else f2_dc<NS, NCH, K1R, EXACT_K, HOT>(mv, sh, off_s, m, k1, rows_s, e_s, &hot);
 }
 
+
+// float32, 8 < k1 <= 16, d <= 128 (NS <= 2): all k1 output rows in ONE register group
+// (16 x 2 float2 = 64 registers), so each input's scores take one pass over its staged row,
+// one 32-value butterfly per input pair and one dA scatter, where the two-group body takes
+// two of each; error rows are padded to 16 floats.
+template <int NS, int NCH, int K1R, bool HOT = false>
+__device__ __forceinline__ void window_update_f2w(const ModelView<float> &mv, const uint32_t *off_s,
+                                                  int m, int k1, float alpha, bool exact,
+                                                  const float *sig_s, bool want_loss,
+                                                  double &loss_acc, long long &cell_acc,
+                                                  float *rows_s, float *e_s, int lane,
+                                                  HotSink<NS> &hot) {
+  static_assert(NS <= 2 && K1R <= 16, "wide body: d <= 128");
+  const F2Shape<NS, NCH> sh(mv, lane);
+  f2_issue_a<NS, NCH>(mv, sh, off_s, m, rows_s);
+  float2 c[K1R][NS];
+  f2_load_c<NS, NCH, K1R, false>(c, mv, sh, off_s + m, k1);
+  f2_score_da<NS, NCH, K1R, false, HOT, 16>(c, mv, sh, off_s, m, k1, alpha, exact, sig_s, want_loss,
+                                            loss_acc, cell_acc, rows_s, e_s, hot);
+  if (m <= 12) f2_dc_io<NS, NCH, K1R, false, HOT, 16>(mv, sh, off_s, m, k1, rows_s, e_s, &hot);
+  else f2_dc<NS, NCH, K1R, false, HOT, 16>(mv, sh, off_s, m, k1, rows_s, e_s, &hot);
+}
 
 // float32, 8 < k1 <= 16, d <= 512: window_update_f2 over two groups of output rows
 // (k < 8, then 8 <= k < k1; kbase shifts the label so only k = 0 is positive).  The

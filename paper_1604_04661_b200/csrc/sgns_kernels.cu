@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -47,17 +48,18 @@ struct Slab {
 };
 // MODE_F2: float32 fast path (only the m input rows are staged); MODE_SMEM: all rows staged
 // MODE_F2S: float32 8 < k1 <= 16, all rows staged; MODE_F2G: the same k1 in two register groups
-enum { MODE_SMEM = 0, MODE_F2 = 1, MODE_F2S = 2, MODE_F2G = 3 };
+// MODE_F2W: float32 8 < k1 <= 16 at d <= 128, one register group of up to 16 output rows
+enum { MODE_SMEM = 0, MODE_F2 = 1, MODE_F2S = 2, MODE_F2G = 3, MODE_F2W = 4 };
 // hot_rows: shared-memory hot-row sink rows of update_windows (H_in + H_out rows, see HotSink)
 // ld: stride of the staged rows (ModelView::lds); hot_ld: of the hot-row sinks (the HBM stride)
 __host__ __device__ inline Slab slab_layout(int mode, int64_t elem, int64_t ld, int mcap, int k1,
                                             int kept_cap, int hot_rows = 0, int64_t hot_ld = 0) {
   Slab s;
   s.rows = 0;
-  const bool a_only = mode == MODE_F2 || mode == MODE_F2G;  // only the input rows are staged
+  const bool a_only = mode == MODE_F2 || mode == MODE_F2G || mode == MODE_F2W;  // only the input rows are staged
   s.e = round32((int64_t)(a_only ? mcap : mcap + k1) * ld * elem);
   // error rows: padded to 8 floats (F2, F2G per group), 16 (F2S), k1 (generic)
-  const int erow = mode == MODE_F2S ? 16 : mode == MODE_F2G ? 8 : (k1 > 8 ? k1 : 8);
+  const int erow = (mode == MODE_F2S || mode == MODE_F2W) ? 16 : mode == MODE_F2G ? 8 : (k1 > 8 ? k1 : 8);
   // F2 / F2G keep only the scaled errors; the other bodies keep raw and scaled
   s.ids = s.e + round32((int64_t)(a_only ? 1 : 2) * mcap * erow * elem);
   s.roff = s.ids + round32((int64_t)(mcap + k1) * 4);
@@ -113,6 +115,11 @@ __device__ __forceinline__ void run_window(const ModelView<T> &mv, const int *id
     for (int r = lane; r < m + k1; r += 32) roff_s[r] = (uint32_t)ids_s[r] * (uint32_t)mv.ld;
     __syncwarp();
     window_update_f2g<NS, NCH, K1R, HOT>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss, cells,
+                                         rows_s, e_s, lane, hot);
+  } else if constexpr (MODE == MODE_F2W) {
+    for (int r = lane; r < m + k1; r += 32) roff_s[r] = (uint32_t)ids_s[r] * (uint32_t)mv.ld;
+    __syncwarp();
+    window_update_f2w<NS, NCH, K1R, HOT>(mv, roff_s, m, k1, alpha, exact, sig_s, want, loss, cells,
                                          rows_s, e_s, lane, hot);
   } else if constexpr (MODE == MODE_F2S) {
     for (int r = lane; r < m + k1; r += 32) roff_s[r] = (uint32_t)ids_s[r] * (uint32_t)mv.ld;
@@ -198,7 +205,7 @@ __global__ void __maxnreg__((UpdRegs<MODE, NS, K1R>::v)) update_windows_kernel(U
                                            sig_s, want, loss, cells, rows_s, e_s, lane, hot);
   }
 
-  if constexpr (HOT && (MODE == MODE_F2 || MODE == MODE_F2S || MODE == MODE_F2G)) {
+  if constexpr (HOT && (MODE == MODE_F2 || MODE == MODE_F2S || MODE == MODE_F2G || MODE == MODE_F2W)) {
     // the warp's sums: one scatter per hot row, none for a row it never updated
     auto flush = [&](const float2 (&v)[NS], float *row) {
       bool any = false;
@@ -655,26 +662,56 @@ static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
   int rc = choose_wpb(kern, table_bytes(sizeof(T)), L.total, &wpb, &bps);
   if (rc) return rc;
   a.hot_in = a.hot_out = 0;
-  if constexpr (HOT && (MODE == MODE_F2 || MODE == MODE_F2G)) {
-    // the largest shared-memory hot-row sink that keeps every resident warp: rows [0, H) of
-    // both matrices (H <= 8), else M_out's row 0 beside the register sink for M_in's row 0
+  if constexpr (HOT && (MODE == MODE_F2 || MODE == MODE_F2G || MODE == MODE_F2W)) {
+    // shared-memory hot-row sinks: rows [0, H) of both matrices (H <= 8), else M_out's row 0
+    // beside the register sink for M_in's row 0
     const int cand[5][2] = {{8, 8}, {4, 4}, {2, 2}, {1, 1}, {0, 1}};
-    for (const auto &hc : cand) {
-      const Slab Lh = slab_layout(MODE, sizeof(T), a.mv.lds, a.mcap, a.k1, 0, hc[0] + hc[1], a.mv.ld);
-      int wh = 0, bh = 0;
-      if (choose_wpb(kern, table_bytes(sizeof(T)), Lh.total, &wh, &bh) == 0 && wh * bh >= wpb * bps) {
-        a.hot_in = hc[0];
-        a.hot_out = hc[1];
-        L = Lh;
-        wpb = wh;
-        bps = bh;
-        break;
-      }
+    // Per-warp sink rows vs resident warps (measured over the configs[1] grid with every
+    // sink forced, profiles/round2_microbench_sinks.jsonl): the step from row 0 alone to rows
+    // [0, 2) of both matrices is worth a quarter of the resident warps while >= 12 stay
+    // (d = 300, w = 5, K = 5: 0.78 -> 0.96 of the copy peak at 12 instead of 16 warps); larger
+    // sinks only pay when they cost no further warp.  So: the largest sink that keeps every
+    // warp; if that is below 2 + 2 rows, a launch with at least 4 windows per resident warp
+    // (d = 300, K = 5: 16,384 windows 0.62 -> 0.76, 4,096 windows 0.43 -> 0.40) may drop to >= max(12, 3/4) of the warps to reach 2 + 2; then the largest sink at that
+    // warp count.  SGNS_UPDATE_HOT=hin,hout forces one candidate (experiments).
+    int forced[2] = {-1, -1};
+    if (const char *fh = std::getenv("SGNS_UPDATE_HOT")) std::sscanf(fh, "%d,%d", &forced[0], &forced[1]);
+    int cw[5], cb[5];
+    Slab cl[5];
+    for (int c = 0; c < 5; ++c) {
+      cl[c] = slab_layout(MODE, sizeof(T), a.mv.lds, a.mcap, a.k1, 0, cand[c][0] + cand[c][1], a.mv.ld);
+      if (choose_wpb(kern, table_bytes(sizeof(T)), cl[c].total, &cw[c], &cb[c]) != 0) cw[c] = cb[c] = 0;
+    }
+    const int wmax = wpb * bps;
+    int need = wmax, pick = -1;
+    for (int c = 0; c < 5 && pick < 0; ++c)
+      if (cw[c] * cb[c] >= need) pick = c;
+    if ((pick < 0 || cand[pick][0] < 2) && cw[2] * cb[2] >= std::max(12, (3 * wmax + 3) / 4) &&
+        (int64_t)a.n_win >= (int64_t)4 * wmax * num_sms()) {
+      need = cw[2] * cb[2];
+      pick = -1;
+      for (int c = 0; c < 5 && pick < 0; ++c)
+        if (cw[c] * cb[c] >= need) pick = c;
+    }
+    if (forced[0] >= 0) {
+      pick = -1;
+      for (int c = 0; c < 5; ++c)
+        if (cand[c][0] == forced[0] && cand[c][1] == forced[1] && cw[c] > 0) pick = c;
+    }
+    if (pick >= 0) {
+      a.hot_in = cand[pick][0];
+      a.hot_out = cand[pick][1];
+      L = cl[pick];
+      wpb = cw[pick];
+      bps = cb[pick];
     }
   }
   a.wpb = wpb;
   const int64_t bytes = table_bytes(sizeof(T)) + (int64_t)wpb * L.total;
   if ((rc = prepare(kern, bytes))) return rc;
+  if (std::getenv("SGNS_UPDATE_DEBUG"))
+    std::fprintf(stderr, "update_windows: mode %d NS %d K1R %d hot %d | mcap %d k1 %d | sink %d+%d rows, %d warps x %d blocks per SM, %lld B\n",
+                 MODE, NS, K1R, (int)HOT, a.mcap, a.k1, a.hot_in, a.hot_out, wpb, bps, (long long)bytes);
   const int64_t blocks_needed = (a.n_win + wpb - 1) / wpb;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)num_sms() * bps));
   kern<<<grid, wpb * 32, bytes, st>>>(a);
@@ -801,6 +838,18 @@ static int update_f2s(UpdateArgs<float> a, cudaStream_t st) {
   // both keep 16 warps per SM at d = 300, +4..12% at d = 100 / 200 with w <= 5, 1.3-1.9x
   // where staging the output rows costs resident warps), so it is the choice; "s" forces F2S.
   const bool staged = force && force[0] == 's';
+  if constexpr (NS <= 2) {
+    // d <= 128: all k1 output rows fit one register group (the wide body: configs[1] d = 100,
+    // K = 10: +6..13% over F2G, K = 15: +2.4% at w <= 5, -6% at w = 10, which stays on F2G);
+    // "g" forces F2G, "w" the wide body
+    if (force ? force[0] == 'w' : !(a.k1 > 12 && a.mcap > 12)) {
+      if (a.k1 <= 12)
+        return hot ? launch_update_t<float, MODE_F2W, NS, NCH, 12, true>(a, st)
+                   : launch_update_t<float, MODE_F2W, NS, NCH, 12, false>(a, st);
+      return hot ? launch_update_t<float, MODE_F2W, NS, NCH, 16, true>(a, st)
+                 : launch_update_t<float, MODE_F2W, NS, NCH, 16, false>(a, st);
+    }
+  }
   if (staged)
     return hot ? launch_update_t<float, MODE_F2S, NS, NCH, 16, true>(a, st)
                : launch_update_t<float, MODE_F2S, NS, NCH, 16, false>(a, st);

@@ -267,6 +267,14 @@ def test_snapshot_configs1_grid(D, w, k):
     _p3_snapshot("f32", D, k, m_fixed=2 * w, n_win=300)
 
 
+@pytest.mark.parametrize("D,k,m", [(100, 15, 20), (128, 12, 7), (36, 9, 20)])
+def test_snapshot_wide_body_forced(D, k, m, monkeypatch):
+    """The d <= 128 single-group body (window_update_f2w) on shapes the launcher would give
+    to the two-group body (K + 1 > 12 with more than 12 inputs) or to other row widths."""
+    monkeypatch.setenv("SGNS_UPDATE_BODY", "w")
+    _p3_snapshot("f32", D, k, m_fixed=m, n_win=300)
+
+
 def _p3_snapshot(dtype, D, k, m_fixed=None, n_win=400):
     P, O = _pkg(), _oracle()
     from paper_1604_04661_b200.kernel_batched import DeviceWindowBatch, WindowBatch
