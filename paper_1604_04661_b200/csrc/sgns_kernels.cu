@@ -145,16 +145,21 @@ template <typename T> struct UpdateArgs {
   int32_t *error;
   int wpb;
   int hot_in, hot_out;  // shared-memory hot-row sink rows (HOT launches; hot_in 0: register sink)
+  int mstage;           // input rows staged at once (= mcap; less: snapshot windows run in chunks)
 };
 
 // Register budget of update_windows_kernel: 128 (16 warps per SM) for the register-row
 // float32 bodies, except 7-8 output rows of >= 5 slots (d > 256) -- F2G's first group always
 // has 8 -- which get up to 168 (12-13 warps) instead of spilling, as the fast driver does;
 // the all-staged generic body 255.
-template <int MODE, int NS, int K1R> struct UpdRegs {
+// d <= 128 with K + 1 <= 6 needs 87-103 registers depending on unrelated code around the body;
+// capped at 96 it keeps 20 resident warps (configs[1] d = 100, K = 5: 0.51-0.56 at 16 warps ->
+// 0.57-0.62 at 20), without spills.
+template <int MODE, int NS, int K1R, bool DRIVER = false> struct UpdRegs {
   static constexpr int v = MODE == MODE_SMEM ? 255
                            : ((MODE == MODE_F2 && K1R >= 7) || MODE == MODE_F2G) && NS >= 5
-                               ? SGNS_FAST_MAXNREG_WIDE : 128;
+                               ? SGNS_FAST_MAXNREG_WIDE
+                               : (!DRIVER && MODE == MODE_F2 && NS <= 2 && K1R <= 6) ? 96 : 128;
 };
 template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT>
 __global__ void __maxnreg__((UpdRegs<MODE, NS, K1R>::v)) update_windows_kernel(UpdateArgs<T> p) {
@@ -162,7 +167,7 @@ __global__ void __maxnreg__((UpdRegs<MODE, NS, K1R>::v)) update_windows_kernel(U
   T *sig_s = reinterpret_cast<T *>(smem);
   load_table(sig_s, p.sig);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Slab L = slab_layout(MODE, sizeof(T), p.mv.lds, p.mcap, p.k1, 0, HOT ? p.hot_in + p.hot_out : 0, p.mv.ld);
+  const Slab L = slab_layout(MODE, sizeof(T), p.mv.lds, p.mstage, p.k1, 0, HOT ? p.hot_in + p.hot_out : 0, p.mv.ld);
   unsigned char *base = smem + table_bytes(sizeof(T)) + (int64_t)warp * L.total;
   T *rows_s = reinterpret_cast<T *>(base + L.rows);
   T *e_s = reinterpret_cast<T *>(base + L.e);
@@ -197,12 +202,19 @@ __global__ void __maxnreg__((UpdRegs<MODE, NS, K1R>::v)) update_windows_kernel(U
       if (lane == 0 && p.error) atomicExch(p.error, 1);
       continue;
     }
-    for (int r = lane; r < m + p.k1; r += 32)
-      ids_s[r] = r < m ? p.in_ids[lo + r] : p.out_ids[(int64_t)w * p.k1 + (r - m)];
-    __syncwarp();
     const bool want = p.loss_every > 0 && (w % p.loss_every) == 0;
-    run_window<T, MODE, NS, NCH, K1R, HOT>(p.mv, ids_s, roff_s, m, p.k1, p.alpha[w], p.exact != 0,
-                                           sig_s, want, loss, cells, rows_s, e_s, lane, hot);
+    // mstage < mcap (snapshot mode only, see launch_update_t): the window runs as chunks of
+    // its inputs against the same outputs -- every gradient comes from the snapshot, so the
+    // chunks are independent and their dC parts add up
+    for (int c0 = 0; c0 < m; c0 += p.mstage) {
+      const int mc = min(p.mstage, m - c0);
+      for (int r = lane; r < mc + p.k1; r += 32)
+        ids_s[r] = r < mc ? p.in_ids[lo + c0 + r] : p.out_ids[(int64_t)w * p.k1 + (r - mc)];
+      __syncwarp();
+      run_window<T, MODE, NS, NCH, K1R, HOT>(p.mv, ids_s, roff_s, mc, p.k1, p.alpha[w], p.exact != 0,
+                                             sig_s, want, loss, cells, rows_s, e_s, lane, hot);
+      __syncwarp();
+    }
   }
 
   if constexpr (HOT && (MODE == MODE_F2 || MODE == MODE_F2S || MODE == MODE_F2G || MODE == MODE_F2W)) {
@@ -286,7 +298,7 @@ struct SmBatch {
 };
 
 template <typename T, int MODE, int NS, int NCH, int K1R, int RNG>
-__global__ void __maxnreg__((UpdRegs<MODE, NS, K1R>::v)) drive_kernel(DriveArgs<T> p) {
+__global__ void __maxnreg__((UpdRegs<MODE, NS, K1R, true>::v)) drive_kernel(DriveArgs<T> p) {
   extern __shared__ __align__(128) unsigned char smem[];
   T *sig_s = reinterpret_cast<T *>(smem);
   load_table(sig_s, p.sig);
@@ -657,11 +669,36 @@ static bool snapshot_mode(const ModelView<float> &mv) {
 template <typename T, int MODE, int NS, int NCH, int K1R, bool HOT = false>
 static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
   auto kern = update_windows_kernel<T, MODE, NS, NCH, K1R, HOT>;
-  Slab L = slab_layout(MODE, sizeof(T), a.mv.lds, a.mcap, a.k1, 0);
+  a.mstage = a.mcap;
+  Slab L = slab_layout(MODE, sizeof(T), a.mv.lds, a.mstage, a.k1, 0);
   int wpb = 0, bps = 0;
   int rc = choose_wpb(kern, table_bytes(sizeof(T)), L.total, &wpb, &bps);
   if (rc) return rc;
   a.hot_in = a.hot_out = 0;
+  if constexpr (HOT) {
+    // Snapshot mode, long windows (w = 10: 20 input rows, 24 KB per warp at d = 300) whose
+    // staging leaves fewer than 16 resident warps: stage half the inputs at a time (kernel:
+    // chunks) if that raises the warp count.  The output rows are loaded and their dC
+    // scattered once per chunk, which costs less than the warps and the larger sink they
+    // leave room for (configs[1] w = 10, K = 5 / 10 / 15: d = 300 0.68 / 0.46 / 0.44 ->
+    // 0.86 / 0.56 / 0.49 at 12 instead of 8 warps; d = 200 0.65 / 0.43 / 0.40 -> 0.77 /
+    // 0.48 / 0.43 at 16 instead of 12; d = 100 keeps 16 warps either way and loses 2-7%,
+    // so it is not split; profiles/round2_microbench_split.jsonl).  SGNS_UPDATE_SPLIT=0/1
+    // forces it off / on (experiments).
+    const char *sp = std::getenv("SGNS_UPDATE_SPLIT");
+    const bool split = sp ? sp[0] == '1' : (a.mcap > 12 && wpb * bps < 16);
+    if (split && a.mcap > 1) {
+      const int half = (a.mcap + 1) / 2;
+      const Slab Ls = slab_layout(MODE, sizeof(T), a.mv.lds, half, a.k1, 0);
+      int ws = 0, bs = 0;
+      if (choose_wpb(kern, table_bytes(sizeof(T)), Ls.total, &ws, &bs) == 0 && (ws * bs > wpb * bps || sp)) {
+        a.mstage = half;
+        L = Ls;
+        wpb = ws;
+        bps = bs;
+      }
+    }
+  }
   if constexpr (HOT && (MODE == MODE_F2 || MODE == MODE_F2G || MODE == MODE_F2W)) {
     // shared-memory hot-row sinks: rows [0, H) of both matrices (H <= 8), else M_out's row 0
     // beside the register sink for M_in's row 0
@@ -679,7 +716,7 @@ static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
     int cw[5], cb[5];
     Slab cl[5];
     for (int c = 0; c < 5; ++c) {
-      cl[c] = slab_layout(MODE, sizeof(T), a.mv.lds, a.mcap, a.k1, 0, cand[c][0] + cand[c][1], a.mv.ld);
+      cl[c] = slab_layout(MODE, sizeof(T), a.mv.lds, a.mstage, a.k1, 0, cand[c][0] + cand[c][1], a.mv.ld);
       if (choose_wpb(kern, table_bytes(sizeof(T)), cl[c].total, &cw[c], &cb[c]) != 0) cw[c] = cb[c] = 0;
     }
     const int wmax = wpb * bps;
@@ -710,8 +747,8 @@ static int launch_update_t(UpdateArgs<T> a, cudaStream_t st) {
   const int64_t bytes = table_bytes(sizeof(T)) + (int64_t)wpb * L.total;
   if ((rc = prepare(kern, bytes))) return rc;
   if (std::getenv("SGNS_UPDATE_DEBUG"))
-    std::fprintf(stderr, "update_windows: mode %d NS %d K1R %d hot %d | mcap %d k1 %d | sink %d+%d rows, %d warps x %d blocks per SM, %lld B\n",
-                 MODE, NS, K1R, (int)HOT, a.mcap, a.k1, a.hot_in, a.hot_out, wpb, bps, (long long)bytes);
+    std::fprintf(stderr, "update_windows: mode %d NS %d K1R %d hot %d | mcap %d k1 %d | sink %d+%d rows, %d warps x %d blocks per SM, %lld B, stage %d\n",
+                 MODE, NS, K1R, (int)HOT, a.mcap, a.k1, a.hot_in, a.hot_out, wpb, bps, (long long)bytes, a.mstage);
   const int64_t blocks_needed = (a.n_win + wpb - 1) / wpb;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)num_sms() * bps));
   kern<<<grid, wpb * 32, bytes, st>>>(a);
@@ -1255,7 +1292,7 @@ int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, cons
     a.sig = static_cast<const float *>(d_sig_table);
     a.exact = sigmoid_mode == SGNS_SIGMOID_EXACT;
     a.loss_every = loss_every; a.loss_sum = d_loss_sum; a.loss_cells = d_loss_cells;
-    a.error = d_error; a.wpb = 1; a.hot_in = a.hot_out = 0;
+    a.error = d_error; a.wpb = 1; a.hot_in = a.hot_out = 0; a.mstage = max_inputs;
     if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
     return update_f32(a, st);
   }
@@ -1270,7 +1307,7 @@ int sgns_update_windows(int32_t dtype, void *d_m_in_dst, void *d_m_out_dst, cons
     a.sig = static_cast<const double *>(d_sig_table);
     a.exact = sigmoid_mode == SGNS_SIGMOID_EXACT;
     a.loss_every = loss_every; a.loss_sum = d_loss_sum; a.loss_cells = d_loss_cells;
-    a.error = d_error; a.wpb = 1; a.hot_in = a.hot_out = 0;
+    a.error = d_error; a.wpb = 1; a.hot_in = a.hot_out = 0; a.mstage = max_inputs;
     if (nch_for(a.mv.nvec) < 0) return SGNS_E_SHAPE;
     return update_f64(a, st);
   }

@@ -275,6 +275,15 @@ def test_snapshot_wide_body_forced(D, k, m, monkeypatch):
     _p3_snapshot("f32", D, k, m_fixed=m, n_win=300)
 
 
+@pytest.mark.parametrize("D,k,m", [(100, 5, 20), (300, 5, 13), (64, 12, 15), (300, 15, 20), (200, 10, 3)])
+def test_snapshot_input_chunks_forced(D, k, m, monkeypatch):
+    """Snapshot-mode launches may stage a long window's inputs in two chunks against the same
+    outputs (launch_update_t: when 20 staged rows cost resident warps); forced here on shapes
+    the launcher would not split, with odd and short windows."""
+    monkeypatch.setenv("SGNS_UPDATE_SPLIT", "1")
+    _p3_snapshot("f32", D, k, m_fixed=m, n_win=300)
+
+
 def _p3_snapshot(dtype, D, k, m_fixed=None, n_win=400):
     P, O = _pkg(), _oracle()
     from paper_1604_04661_b200.kernel_batched import DeviceWindowBatch, WindowBatch
